@@ -1,0 +1,267 @@
+/*
+ * valve_cuda.h -- the C-ABI drop-in boundary of the B200 colocation hot path.
+ *
+ * Everything behind these entry points runs as sm_100a CUDA kernels on the pool's
+ * device (libvalve.so, built from paper_2604_07874_b200/csrc).  There is no CPU
+ * fallback: creating a pool without a usable CUDA device fails with VALVE_CUDA_ERROR.
+ *
+ * Each entry point replaces one method of the reference runtime API in
+ * /root/reference/proj/include/colosim (cited per function).  Value semantics are the
+ * reference's; C++ exceptions become status codes:
+ *     std::invalid_argument -> VALVE_INVALID_ARGUMENT
+ *     std::out_of_range     -> VALVE_OUT_OF_RANGE   (std::vector::at in the reference)
+ *     std::logic_error      -> VALVE_LOGIC_ERROR
+ *     std::runtime_error    -> VALVE_RUNTIME_ERROR  (also capacity limits of the device tables)
+ *     any CUDA failure      -> VALVE_CUDA_ERROR
+ * and valve_last_error() returns the message (thread-local).  Nothing throws across
+ * this boundary.  include/colosim/*.hpp re-raise the same exception types so callers
+ * written against the reference compile and behave unchanged.
+ *
+ * Sizes: arrays are plain pointers plus explicit capacities.  Output functions
+ * always report the full size; pass a NULL buffer / zero capacity to query it.
+ */
+#ifndef VALVE_CUDA_H
+#define VALVE_CUDA_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  VALVE_OK = 0,
+  VALVE_INVALID_ARGUMENT = 1,
+  VALVE_LOGIC_ERROR = 2,
+  VALVE_RUNTIME_ERROR = 3,
+  VALVE_CUDA_ERROR = 4,
+  VALVE_OUT_OF_RANGE = 5,
+};
+
+const char* valve_last_error(void);
+/* Number of CUDA kernels this library launched in this process (all pools, gates, copies). */
+int64_t valve_kernel_launches(void);
+
+/* ================================================================ pool (a1, c1-c3, c5) */
+/* Replaces colosim::MemoryPool (memory.hpp:19-98).  Device layout: see DESIGN.md §3. */
+typedef struct valve_pool valve_pool;
+
+typedef struct {
+  int device;                 /* CUDA ordinal */
+  int total_handles;          /* memory.hpp:23 */
+  int handle_size_pages;      /* <= 256 */
+  int page_size_tokens;
+  int64_t slot_bytes;         /* physical bytes per page slot; 0 = no page store (decisions only) */
+  int64_t page_bytes;         /* bytes of KV actually held per page (<= slot_bytes) */
+  int max_requests;           /* live offline requests the device request table holds */
+  int max_pages_per_request;  /* block-table row length */
+} valve_pool_config;
+
+/* Defaults: device 0, slot_bytes 0, page_bytes 0, max_requests 4096, max_pages 4096. */
+void valve_pool_config_default(valve_pool_config* cfg);
+/* memory.hpp:23 MemoryPool(total_handles, handle_size_pages, page_size_tokens) */
+int valve_pool_create(int total_handles, int handle_size_pages, int page_size_tokens, valve_pool** out);
+int valve_pool_create_ex(const valve_pool_config* cfg, valve_pool** out);
+void valve_pool_destroy(valve_pool* p);
+
+/* out = {free_handles, online_handles, offline_handles, online_used_pages,
+ *        online_capacity_pages}  (memory.hpp:28-41) */
+int valve_pool_counts(const valve_pool* p, int64_t out[5]);
+int valve_pool_geometry(const valve_pool* p, int out[4]); /* H, S, page_tokens, quarantine id */
+int64_t valve_pool_quarantine_page_id(const valve_pool* p); /* memory.hpp:33-35 */
+
+int valve_pool_online_grow(valve_pool* p, int k, int64_t t);            /* memory.hpp:43 */
+int valve_pool_online_release(valve_pool* p, int k, int* released);    /* memory.hpp:45 */
+int valve_pool_online_use_pages(valve_pool* p, int64_t n);             /* memory.hpp:47 */
+int valve_pool_online_free_pages(valve_pool* p, int64_t n);            /* memory.hpp:48 */
+int valve_pool_offline_reserve(valve_pool* p, int64_t req, int pages, int64_t t,
+                               int max_offline_handles, int* ok);      /* memory.hpp:54 */
+int valve_pool_offline_release(valve_pool* p, int64_t req);            /* memory.hpp:56 */
+int valve_pool_requests_on_handle(const valve_pool* p, int handle, int64_t* out, int cap,
+                                  int* n);                             /* memory.hpp:57 */
+int valve_pool_handles_of_request(const valve_pool* p, int64_t req, int* out, int cap,
+                                  int* n);                             /* memory.hpp:58 */
+int valve_pool_offline_pages_of(const valve_pool* p, int64_t req, int* out); /* memory.hpp:59 */
+/* memory.hpp:62 snapshot(): CSR ids[nh], mapped_at[nh], off[nh+1], reqs[nr] */
+int valve_pool_snapshot(const valve_pool* p, int* ids, int64_t* mapped_at, int* off, int64_t* reqs,
+                        int cap_h, int cap_r, int* nh, int* nr);
+/* memory.hpp:64-71 apply_reclaim().  handles[n_handles]; evicted[n_evicted] ascending;
+ * inv_off[n_evicted+1] CSR into inv_pages (logical ids the reference reports, ascending per
+ * request).  inv_phys / inv_blk (may be NULL) are aligned with inv_pages: the physical page
+ * the bytes live in, and the page's block index inside its request.  The device keeps the
+ * physical list for valve_pool_reclaim_copy(). */
+int valve_pool_apply_reclaim(valve_pool* p, const int* ids, int k, int64_t t, int* handles,
+                             int* n_handles, int64_t* evicted, int* n_evicted, int* inv_off,
+                             int64_t* inv_pages, int* inv_phys, int* inv_blk, int cap_ev,
+                             int cap_pages, int* n_pages);
+int valve_pool_handle_state(const valve_pool* p, int handle, int* state);      /* memory.hpp:73 */
+int valve_pool_handle_mapped_at(const valve_pool* p, int handle, int64_t* t);  /* memory.hpp:74 */
+int valve_pool_check_invariants(const valve_pool* p);                          /* memory.hpp:78 */
+/* Block table of a live offline request: physical page ids in block order. */
+int valve_pool_block_table(const valve_pool* p, int64_t req, int* out, int cap, int* n);
+
+/* ------------------------------------------------- fused device reclaim (a2+a3+a5 on-device) */
+/* Recompute costs (requests.hpp:68-69, sim.cpp:877-883) kept next to each request row. */
+int valve_pool_set_costs(valve_pool* p, int n, const int64_t* reqs, const int64_t* costs);
+enum { VALVE_SELECT_SELECTIVE = 0, VALVE_SELECT_FIFO = 1, VALVE_SELECT_ORACLE = 2 };
+/* snapshot -> selection (mode) -> apply_reclaim in ONE kernel launch, no host round trip in
+ * between (sim.cpp:936-942).  Results stay on the device for valve_pool_reclaim_copy();
+ * the summary (n_handles, n_evicted, n_pages) is returned; use
+ * valve_pool_last_reclaim() to read the full result. */
+int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles, int* n_evicted,
+                       int* n_pages);
+int valve_pool_last_reclaim(const valve_pool* p, int* handles, int64_t* evicted, int* inv_off,
+                            int64_t* inv_pages, int* inv_phys, int* inv_blk, int cap_h, int cap_ev,
+                            int cap_pages);
+
+/* ------------------------------------------------------------- reclaim copy (a6) */
+typedef struct {
+  int ctas;                 /* copy CTAs (keep small so online keeps the SMs); 0 = default */
+  int threads;              /* threads per CTA; 0 = default */
+  int64_t chunk_bytes;      /* work unit; 0 = default (64 KiB) */
+  double rate_bytes_per_s;  /* rate bound; <= 0 = unbounded */
+  int64_t burst_bytes;      /* token-bucket depth for the rate bound */
+  int use_tma;              /* 1 = stage chunks through shared memory with cp.async.bulk */
+} valve_copy_params;
+typedef struct {
+  int64_t bytes;
+  int64_t pages;
+  double kernel_ms;         /* CUDA-event time of the copy kernel */
+  uint64_t t_first_ns;      /* %globaltimer at the first chunk issue */
+  uint64_t t_last_ns;       /* %globaltimer at the last chunk's stores retired */
+} valve_copy_stats;
+void valve_copy_params_default(valve_copy_params* c);
+/* Gathers the pages invalidated by the last apply/reclaim, in report order, into pinned
+ * host memory (cudaHostAlloc'd or cudaHostRegister'd; dst_bytes >= n_pages*page_bytes).
+ * Synchronous. */
+int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
+                            const valve_copy_params* params, valve_copy_stats* stats);
+/* Pinned, device-mapped host staging for reclaimed pages (cudaHostAlloc, mapped). */
+int valve_host_alloc(int64_t bytes, void** out);
+void valve_host_free(void* p);
+/* Same copy through the copy engines (cudaMemcpyAsync per page) -- the baseline. */
+int valve_pool_reclaim_copy_ce(valve_pool* p, void* host_dst, int64_t dst_bytes,
+                               valve_copy_stats* stats);
+/* Writes the deterministic image of every live offline page (request, block) into its
+ * physical slot; models the offline engine having written its KV. */
+int valve_pool_fill_pages(valve_pool* p);
+/* Raw device pointers for kernels of the offline engine. */
+typedef struct {
+  void* pages;          /* slot_bytes * H * S bytes */
+  int* block_tables;    /* [max_requests][max_pages_per_request] physical page ids */
+  int64_t slot_bytes, page_bytes;
+  int max_pages_per_request;
+  int quarantine_page;
+  void* stream;         /* the pool's cudaStream_t */
+} valve_pool_view;
+int valve_pool_view_get(const valve_pool* p, valve_pool_view* v);
+/* Row of a live request in block_tables (or -1). */
+int valve_pool_request_row(const valve_pool* p, int64_t req, int* row);
+
+/* ========================================================= selection over host instances (a3,a4) */
+/* reclaim.hpp:28-37.  Instance as CSR (ids, mapped_at, off, reqs); costs as sorted unique
+ * keys/values (the std::map of reclaim.hpp:25).  Runs on `device`. */
+int valve_select(int device, int n, const int* ids, const int64_t* mapped_at, const int* off,
+                 const int64_t* reqs, int m, const int64_t* cost_keys, const int64_t* cost_vals,
+                 int k, int mode, int* out, int* n_out);
+int valve_evicted_cost(int device, int n, const int* ids, const int* off, const int64_t* reqs, int m,
+                       const int64_t* cost_keys, const int64_t* cost_vals, const int* pick,
+                       int n_pick, int64_t* cost);
+
+/* ============================================================= reservation controller (c4) */
+/* memory.hpp:103-146: fp64 control plane, host-resident by design (north star (c)). */
+typedef struct {
+  double alpha, beta;
+  int64_t t_init_us, delta_us, t_min_us, t_max_us, window_us;
+  double target_per_window;
+  int h_min;
+  double pressure_threshold;
+} valve_resparams;
+typedef struct valve_resctl valve_resctl;
+void valve_resparams_default(valve_resparams* p);
+int valve_resctl_create(const valve_resparams* p, valve_resctl** out);
+void valve_resctl_destroy(valve_resctl* c);
+int64_t valve_resctl_interval(const valve_resctl* c);
+int64_t valve_resctl_pressure_events(const valve_resctl* c);
+int valve_resctl_grow_target(const valve_resctl* c, int h, int cap);
+void valve_resctl_record_pressure(valve_resctl* c, int64_t t);
+int valve_resctl_release_due(const valve_resctl* c, int64_t t, int h);
+void valve_resctl_note_tick(valve_resctl* c, int64_t t);
+int64_t valve_resctl_window_tick(valve_resctl* c, int64_t t);
+int64_t valve_resctl_pressure_in_window(const valve_resctl* c, int64_t t);
+
+/* ======================================================== device preemption gate (b1, b4) */
+/* An HBM gate word {generation, closed} polled by every warp of the gated offline
+ * kernels at each tile boundary; quiesce is acknowledged per CTA. */
+typedef struct valve_gate valve_gate;
+typedef struct {
+  uint32_t gen;            /* last generation written */
+  uint32_t closed;
+  uint32_t quiesced_gen;   /* last generation fully acknowledged */
+  uint32_t live_ctas;
+  uint64_t t_first_seen_ns;
+  uint64_t t_quiesced_ns;
+  uint64_t tiles_done;
+  uint64_t canary_hits;    /* reads that resolved to the quarantine page */
+  uint64_t tiles_claimed;  /* the HBM cursor (claims, incl. one overshoot per retiring warp) */
+} valve_gate_state;
+int valve_gate_create(int device, valve_gate** out);
+void valve_gate_destroy(valve_gate* g);
+/* Stream-ordered gate store (cuStreamWriteValue) on `stream` (NULL: the gate's own
+ * high-priority stream).  Takes no SM: works while offline kernels occupy every SM. */
+int valve_gate_raise(valve_gate* g, uint32_t gen, void* stream);
+int valve_gate_release(valve_gate* g, uint32_t gen, void* stream);
+/* Makes `stream` wait (cuStreamWaitValue) until every gated kernel acknowledged `gen`. */
+int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* stream);
+/* TP fan-out: members' gate words are written by the leader over NVLink peer memory. */
+int valve_gate_attach_peers(valve_gate* leader, valve_gate** members, int n);
+int valve_gate_read(const valve_gate* g, valve_gate_state* out);
+void* valve_gate_stream(const valve_gate* g);
+
+/* Gated offline workload (b4): a persistent, tile-looped decode-attention-shaped kernel over
+ * the pool's KV pages through the block tables.  One tile = one (request, page) pair:
+ * q . K over the page as bf16, fp32 accumulate.  Tiles are claimed from an HBM cursor;
+ * a raised gate stops claiming at the next tile boundary and the CTA exits (context save =
+ * the cursor).  Returns immediately (stream-ordered). */
+typedef struct {
+  const int* rows;        /* device: request rows to decode */
+  const int* npages;      /* device: pages per listed request */
+  int n_requests;
+  int64_t total_tiles;    /* sum of npages */
+  float* out;             /* device: one fp32 per tile */
+  int ctas;               /* 0 = 148 x resident */
+  int threads;            /* 0 = 256 */
+  int poll;               /* 0 = no gate polling (overhead baseline) */
+} valve_offline_work;
+int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work* w, void* stream);
+/* Resets the tile cursor / statistics (new work). */
+int valve_offline_reset(valve_gate* g);
+
+/* ============================================================ channel controller (b1, b2) */
+/* channel.hpp:30-80 state machine with C hooks; optionally bound to a device gate so
+ * disable/enable raise/release it (valve_channel_bind_gate). */
+typedef struct {
+  void* user;
+  void (*schedule)(void* user, int64_t when, int64_t gen, int cooldown);
+  void (*on_disabled)(void* user, int64_t t);
+  void (*on_enabled)(void* user, int64_t t);
+  void (*log)(void* user, int64_t t, int what, int64_t aux, int memory_cause);
+} valve_channel_hooks;
+typedef struct valve_channel valve_channel;
+int valve_channel_create(int64_t toggle_us, int64_t cooldown_us, const valve_channel_hooks* hooks,
+                         valve_channel** out);
+void valve_channel_destroy(valve_channel* c);
+int valve_channel_bind_gate(valve_channel* c, valve_gate* g);
+int valve_channel_state(const valve_channel* c);
+int valve_channel_offline_compute_allowed(const valve_channel* c);
+int64_t valve_channel_disables_issued(const valve_channel* c);
+int64_t valve_channel_pending_effective(const valve_channel* c);
+void valve_channel_note_busy(valve_channel* c, int64_t t);
+void valve_channel_note_all_idle(valve_channel* c, int64_t t);
+int64_t valve_channel_ensure_disabled(valve_channel* c, int64_t t);
+void valve_channel_handle_toggle(valve_channel* c, int64_t t, int64_t gen);
+void valve_channel_handle_cooldown(valve_channel* c, int64_t t, int64_t gen);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

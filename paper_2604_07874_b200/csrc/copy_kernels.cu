@@ -1,0 +1,180 @@
+// copy_kernels.cu -- reclaim gather-copy: the pages invalidated by apply_reclaim, in the
+// reference's report order (request ascending, page id ascending; memory.cpp:176-179),
+// from their physical HBM slots into pinned host memory over PCIe.
+//
+// Work unit = one chunk (default 64 KiB) of one page, claimed from an HBM cursor so a few
+// CTAs stream the whole list while the rest of the GPU stays with online work.  Each thread
+// keeps kVec 16-byte loads in flight (ld.global.nc.L1::no_allocate -- the pool is read once),
+// then issues 16-byte stores to the host-mapped destination (posted PCIe writes).  The rate
+// bound is a token bucket on %globaltimer: chunk c may start once
+//   now >= t0 + (c*chunk - burst) * ns_per_byte.
+// No UVM: the destination is cudaHostAlloc'd / registered memory, never managed memory.
+#include "valve_kernels.h"
+
+namespace valve {
+
+namespace {
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_host(uint4* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ unsigned long long start_time(unsigned long long* t_first) {
+  const unsigned long long now = globaltimer_ns();
+  const unsigned long long prev = atomicCAS(t_first, 0ull, now);
+  return prev ? prev : now;
+}
+
+__device__ __forceinline__ void pace(const CopyArgs& A, unsigned long long t0, long long c) {
+  if (A.ns_per_byte <= 0.0) return;
+  const double credit = (double)(c * A.chunk_bytes - A.burst_bytes) * A.ns_per_byte;
+  if (credit <= 0.0) return;
+  const unsigned long long allowed = t0 + (unsigned long long)credit;
+  while (globaltimer_ns() < allowed) __nanosleep(2000);
+}
+
+}  // namespace
+
+constexpr int kVec = 8;
+
+__global__ void __launch_bounds__(512) k_reclaim_copy(CopyArgs A) {
+  __shared__ long long s_chunk;
+  __shared__ unsigned long long s_t0;
+  if (threadIdx.x == 0) s_t0 = start_time(A.t_first);
+  const int64_t cpp = (A.page_bytes + A.chunk_bytes - 1) / A.chunk_bytes;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_chunk = (long long)atomicAdd(A.cursor, 1ull);
+      if (s_chunk < A.n_chunks) pace(A, s_t0, s_chunk);
+    }
+    __syncthreads();
+    const long long c = s_chunk;
+    __syncthreads();
+    if (c >= A.n_chunks) break;
+    const int64_t page = c / cpp;
+    const int64_t off = (c % cpp) * A.chunk_bytes;
+    const int64_t len = min(A.chunk_bytes, A.page_bytes - off);
+    const uint4* src =
+        reinterpret_cast<const uint4*>(A.pages + (int64_t)A.phys[page] * A.slot_bytes + off);
+    uint4* dst = reinterpret_cast<uint4*>(A.dst + page * A.page_bytes + off);
+    const int nvec = (int)(len >> 4);
+    const int step = blockDim.x * kVec;
+    for (int base = 0; base < nvec; base += step) {
+      uint4 v[kVec];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) {
+        const int i = base + u * blockDim.x + threadIdx.x;
+        if (i < nvec) v[u] = ld_stream(src + i);
+      }
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) {
+        const int i = base + u * blockDim.x + threadIdx.x;
+        if (i < nvec) st_host(dst + i, v[u]);
+      }
+    }
+  }
+  // stores retired system-wide before the completion stamp
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(A.t_last, globaltimer_ns());
+}
+
+// Variant staging each chunk through shared memory with the bulk-copy engine:
+// cp.async.bulk global->shared (mbarrier complete_tx), then cp.async.bulk shared->global
+// into the host-mapped destination.  Double-buffered: the load of chunk i+1 overlaps the
+// store of chunk i.
+constexpr int kTmaChunk = 32768;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* g, unsigned bytes, uint64_t* bar) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(s),
+      "l"(g), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* g, const void* smem, unsigned bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(s),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_le1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// One elected thread per CTA drives the bulk engine; chunks of kTmaChunk bytes are claimed
+// in CTA-sized batches from the cursor (the pace() bound applies per claim).
+__global__ void __launch_bounds__(32) k_reclaim_copy_tma(CopyArgs A) {
+  extern __shared__ __align__(128) unsigned char sbuf[];  // 2 x kTmaChunk
+  __shared__ __align__(8) uint64_t bar[2];
+  if (threadIdx.x != 0) return;
+  const unsigned long long t0 = start_time(A.t_first);
+  mbar_init(&bar[0], 1);
+  mbar_init(&bar[1], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int64_t cpp = (A.page_bytes + A.chunk_bytes - 1) / A.chunk_bytes;
+  unsigned phase[2] = {0, 0};
+  int buf = 0;
+  for (;;) {
+    const long long c = (long long)atomicAdd(A.cursor, 1ull);
+    if (c >= A.n_chunks) break;
+    pace(A, t0, c);
+    const int64_t page = c / cpp;
+    const int64_t off0 = (c % cpp) * A.chunk_bytes;
+    const int64_t len = min(A.chunk_bytes, A.page_bytes - off0);
+    const uint8_t* src = A.pages + (int64_t)A.phys[page] * A.slot_bytes + off0;
+    uint8_t* dst = A.dst + page * A.page_bytes + off0;
+    for (int64_t o = 0; o < len; o += kTmaChunk) {
+      const unsigned bytes = (unsigned)min((int64_t)kTmaChunk, len - o);
+      unsigned char* s = sbuf + buf * kTmaChunk;
+      bulk_wait_read_le1();  // the store that last read this buffer has drained
+      mbar_expect_tx(&bar[buf], bytes);
+      bulk_g2s(s, src + o, bytes, &bar[buf]);
+      mbar_wait(&bar[buf], phase[buf]);
+      phase[buf] ^= 1;
+      bulk_s2g(dst + o, s, bytes);
+      buf ^= 1;
+    }
+  }
+  bulk_wait_all();
+  __threadfence_system();
+  atomicMax(A.t_last, globaltimer_ns());
+}
+
+}  // namespace valve

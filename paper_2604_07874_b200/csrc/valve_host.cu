@@ -1,0 +1,1303 @@
+// valve_host.cu -- host side of the C-ABI (include/valve_cuda.h): device allocation,
+// kernel launches on the pool's stream, error translation, and the two host control
+// planes the north star keeps on the CPU (ReservationController, ChannelController state
+// machine).  No exception or CUDA error crosses extern "C".
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/valve_cuda.h"
+#include "valve_kernels.h"
+
+using namespace valve;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+struct Err {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Err{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(VALVE_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return VALVE_OK;
+  } catch (const Err& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return VALVE_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VALVE_RUNTIME_ERROR;
+  }
+}
+
+void counted() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// Driver stream memory operations, fetched through the runtime (no -lcuda link dependency).
+using PFN_write32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using PFN_wait32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using PFN_write64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+struct MemOps {
+  PFN_write32 write32 = nullptr;
+  PFN_wait32 wait32 = nullptr;
+  PFN_write64 write64 = nullptr;
+};
+const MemOps& memops() {
+  static MemOps ops;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuStreamWriteValue32", (void**)&ops.write32, cudaEnableDefault, &q);
+    cudaGetDriverEntryPoint("cuStreamWaitValue32", (void**)&ops.wait32, cudaEnableDefault, &q);
+    cudaGetDriverEntryPoint("cuStreamWriteValue64", (void**)&ops.write64, cudaEnableDefault, &q);
+  });
+  if (!ops.write32 || !ops.wait32 || !ops.write64)
+    fail(VALVE_CUDA_ERROR, "stream memory operations unavailable in this driver");
+  return ops;
+}
+void cu_ck(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) fail(VALVE_CUDA_ERROR, std::string(what) + " failed (CUresult " + std::to_string((int)r) + ")");
+}
+
+int64_t next_pow2(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+const char* detail_msg(int det) {
+  switch (det) {
+    case kDetGrowExceeds: return "online_grow: k exceeds free handles";
+    case kDetRowsFull: return "offline_reserve: device request table full (raise max_requests)";
+    case kDetBlocksFull: return "offline_reserve: request exceeds max_pages_per_request";
+    case kDetNoCost: return "reclaim: request without cost entry";
+    case kDetInvPartition: return "MemoryPool: handle sets do not partition the pool";
+    case kDetInvOnline: return "MemoryPool: online page accounting out of bounds";
+    case kDetInvSlots: return "MemoryPool: slot accounting mismatch";
+    case kDetInvNonOffline: return "MemoryPool: non-offline handle holds offline pages";
+    case kDetInvRow: return "MemoryPool: request page count does not match its slots";
+    case kDetInvBlock: return "MemoryPool: block table does not point back at its slot";
+    default: return "device error";
+  }
+}
+
+}  // namespace
+
+// ===================================================================================== pool
+
+struct valve_pool {
+  valve_pool_config cfg{};
+  int H = 0, S = 0, R = 0, Pblk = 0;
+  cudaStream_t stream = nullptr;
+  PoolDev d{};
+  Mirror* mirror = nullptr;  // pinned host
+  int64_t online_used = 0;   // memory.hpp:97 aggregate (host scalar)
+  int* d_ids = nullptr;      // apply ids upload
+  int64_t* d_in64 = nullptr; // cost upload
+  int64_t* d_in64b = nullptr;
+  size_t smem_snapshot = 0, smem_reclaim = 0;
+  std::vector<void*> dev_allocs;
+  int last_n_handles = 0, last_n_evicted = 0, last_n_pages = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  template <class T>
+  T* dalloc(int64_t n) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(T)), "cudaMalloc");
+    dev_allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+
+  void sync_and_check(const char* op) {
+    ck(cudaGetLastError(), op);
+    ck(cudaStreamSynchronize(stream), op);
+    if (mirror->err) {
+      const int code = mirror->err;
+      const int det = mirror->err_detail;
+      std::string msg;
+      if (det == kDetNotOffline)
+        msg = "apply_reclaim: handle " + std::to_string(mirror->err_arg) + " is not offline-mapped";
+      else if (det == kDetApplyRange)
+        msg = "apply_reclaim: handle " + std::to_string(mirror->err_arg) + " out of range";
+      else
+        msg = detail_msg(det);
+      fail(code, msg);
+    }
+  }
+
+  template <class K, class... Args>
+  void launch1(const char* op, K kernel, size_t smem, Args... args) {
+    ck(cudaSetDevice(cfg.device), "cudaSetDevice");
+    kernel<<<1, kNT, smem, stream>>>(args...);
+    counted();
+    sync_and_check(op);
+  }
+
+  void counts(int64_t out[5]) const {
+    out[0] = mirror->n_free;
+    out[1] = mirror->n_online;
+    out[2] = mirror->n_offline;
+    out[3] = online_used;
+    out[4] = (int64_t)mirror->n_online * S;
+  }
+
+  void d2h(void* dst, const void* src, size_t bytes) {
+    if (!bytes || !dst) return;
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream), "cudaMemcpyAsync");
+  }
+
+  ~valve_pool() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : dev_allocs) cudaFree(p);
+    if (d.pages) cudaFree(d.pages);
+    if (mirror) cudaFreeHost(mirror);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+static void pool_init(valve_pool* p, const valve_pool_config& c) {
+  if (c.total_handles <= 0 || c.handle_size_pages <= 0 || c.page_size_tokens <= 0)
+    fail(VALVE_INVALID_ARGUMENT, "MemoryPool: sizes must be > 0");  // memory.cpp:15
+  if (c.handle_size_pages > 256)
+    fail(VALVE_INVALID_ARGUMENT, "MemoryPool: handle_size_pages > 256 is not supported on device");
+  if ((int64_t)c.total_handles * c.handle_size_pages >= (1 << 24))
+    fail(VALVE_INVALID_ARGUMENT, "MemoryPool: total pages must be < 2^24");
+  if (c.max_requests <= 0 || c.max_requests >= (1 << 16) || c.max_pages_per_request <= 0)
+    fail(VALVE_INVALID_ARGUMENT, "MemoryPool: bad request-table geometry");
+  if (c.slot_bytes < 0 || c.page_bytes < 0 || c.page_bytes > c.slot_bytes || c.page_bytes % 16 ||
+      c.slot_bytes % 16)
+    fail(VALVE_INVALID_ARGUMENT, "MemoryPool: page/slot bytes must be 16-byte multiples, page <= slot");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0)
+    fail(VALVE_CUDA_ERROR, "no CUDA device: the valve pool runs only on the GPU");
+  if (c.device < 0 || c.device >= ndev) fail(VALVE_INVALID_ARGUMENT, "MemoryPool: bad device ordinal");
+  p->cfg = c;
+  p->H = c.total_handles;
+  p->S = c.handle_size_pages;
+  p->R = c.max_requests;
+  p->Pblk = c.max_pages_per_request;
+  ck(cudaSetDevice(c.device), "cudaSetDevice");
+  ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaEventCreate(&p->ev0), "cudaEventCreate");
+  ck(cudaEventCreate(&p->ev1), "cudaEventCreate");
+  const int H = p->H, S = p->S, R = p->R;
+  const int64_t HS = (int64_t)H * S;
+  PoolDev& d = p->d;
+  d.H = H;
+  d.S = S;
+  d.R = R;
+  d.P = p->Pblk;
+  d.HC = (int)next_pow2(2 * (int64_t)R);
+  d.quarantine = (int)HS;
+  d.hstate = p->dalloc<uint8_t>(H);
+  d.hmapped = p->dalloc<int64_t>(H);
+  d.hused = p->dalloc<int>(H);
+  d.slot_row = p->dalloc<int>(HS);
+  d.slot_lid = p->dalloc<int>(HS);
+  d.slot_blk = p->dalloc<int>(HS);
+  d.row_req = p->dalloc<int64_t>(R);
+  d.row_cost = p->dalloc<int64_t>(R);
+  d.row_npages = p->dalloc<int>(R);
+  d.row_nblk = p->dalloc<int>(R);
+  d.bt = p->dalloc<int>((int64_t)R * p->Pblk);
+  d.ht_key = p->dalloc<int64_t>(d.HC);
+  d.ht_row = p->dalloc<int>(d.HC);
+  d.ring = p->dalloc<int>(R);
+  d.hdr = p->dalloc<PoolHdr>(1);
+  const int64_t HSR = std::max<int64_t>(HS, R);
+  d.s_hid = p->dalloc<int>(H);
+  d.s_hmap = p->dalloc<int64_t>(H);
+  d.s_roff = p->dalloc<int>(H + 1);
+  d.s_rref = p->dalloc<int>(HS);
+  d.s_qoff = p->dalloc<int>(R + 1);
+  d.s_qcnt = p->dalloc<int>(HSR);
+  d.s_qh = p->dalloc<int>(HS);
+  d.s_marg = p->dalloc<int64_t>(H);
+  d.s_taken = p->dalloc<int>(H);
+  d.s_ev = p->dalloc<int>(R);
+  d.s_pick = p->dalloc<int>(H);
+  d.s_evrows = p->dalloc<int>(R);
+  d.s_rank = p->dalloc<int>(R);
+  d.s_key = p->dalloc<uint64_t>(next_pow2(HS));
+  d.s_pay = p->dalloc<int>(next_pow2(HS));
+  d.s_cnt = p->dalloc<int>(H);
+  d.s_tphys = p->dalloc<int>(HS);
+  d.s_tblk = p->dalloc<int>(HS);
+  d.res_handles = p->dalloc<int>(H);
+  d.res_evicted = p->dalloc<int64_t>(R);
+  d.res_inv_off = p->dalloc<int>(R + 1);
+  d.res_pages = p->dalloc<int64_t>(HS);
+  d.res_phys = p->dalloc<int>(HS);
+  d.res_blk = p->dalloc<int>(HS);
+  d.res_counts = p->dalloc<int>(4);
+  p->d_ids = p->dalloc<int>(std::max(H, 1) * 2);
+  p->d_in64 = p->dalloc<int64_t>(R);
+  p->d_in64b = p->dalloc<int64_t>(R);
+  d.slot_bytes = c.slot_bytes;
+  d.page_bytes = c.page_bytes;
+  if (c.slot_bytes > 0) {
+    void* pg = nullptr;
+    ck(cudaMalloc(&pg, (size_t)(HS * c.slot_bytes)), "cudaMalloc(page store)");
+    d.pages = static_cast<uint8_t*>(pg);
+  }
+  ck(cudaHostAlloc((void**)&p->mirror, sizeof(Mirror), cudaHostAllocMapped), "cudaHostAlloc");
+  std::memset(p->mirror, 0, sizeof(Mirror));
+  ck(cudaHostGetDevicePointer((void**)&d.mirror, p->mirror, 0), "cudaHostGetDevicePointer");
+  // initial state: all handles free, no slots, empty request table, every row in the ring
+  ck(cudaMemsetAsync(d.hstate, 0, H, p->stream), "memset");
+  ck(cudaMemsetAsync(d.hmapped, 0, H * 8, p->stream), "memset");
+  ck(cudaMemsetAsync(d.hused, 0, H * 4, p->stream), "memset");
+  ck(cudaMemsetAsync(d.slot_row, 0xff, HS * 4, p->stream), "memset");
+  ck(cudaMemsetAsync(d.slot_lid, 0xff, HS * 4, p->stream), "memset");
+  ck(cudaMemsetAsync(d.slot_blk, 0xff, HS * 4, p->stream), "memset");
+  ck(cudaMemsetAsync(d.row_npages, 0, R * 4, p->stream), "memset");
+  ck(cudaMemsetAsync(d.row_nblk, 0, R * 4, p->stream), "memset");
+  ck(cudaMemsetAsync(d.row_cost, 0, R * 8, p->stream), "memset");
+  ck(cudaMemsetAsync(d.bt, 0xff, (size_t)R * p->Pblk * 4, p->stream), "memset");
+  ck(cudaMemsetAsync(d.ht_row, 0xff, (size_t)d.HC * 4, p->stream), "memset");
+  ck(cudaMemsetAsync(d.s_ev, 0, R * 4, p->stream), "memset");
+  std::vector<int> ring(R);
+  for (int i = 0; i < R; ++i) ring[i] = i;
+  ck(cudaMemcpyAsync(d.ring, ring.data(), R * 4, cudaMemcpyHostToDevice, p->stream), "upload");
+  PoolHdr hdr{H, 0, 0, 0, R, 0};
+  ck(cudaMemcpyAsync(d.hdr, &hdr, sizeof hdr, cudaMemcpyHostToDevice, p->stream), "upload");
+  ck(cudaStreamSynchronize(p->stream), "init");
+  p->mirror->n_free = H;
+  // dynamic shared memory of the warp-buffer kernels
+  p->smem_snapshot = (size_t)32 * S * (8 + 4);
+  p->smem_reclaim = (size_t)32 * S * 4;
+  ck(cudaFuncSetAttribute(k_snapshot, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)std::max<size_t>(p->smem_snapshot, 1)),
+     "cudaFuncSetAttribute");
+  ck(cudaFuncSetAttribute(k_reclaim, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)std::max<size_t>(p->smem_reclaim, 1)),
+     "cudaFuncSetAttribute");
+}
+
+namespace {
+
+void read_apply_results(valve_pool* p, int* handles, int64_t* evicted, int* inv_off, int64_t* pages,
+                        int* phys, int* blk, int cap_h, int cap_ev, int cap_pages) {
+  const int nh = p->last_n_handles, ne = p->last_n_evicted, np = p->last_n_pages;
+  if (handles) p->d2h(handles, p->d.res_handles, (size_t)std::min(nh, cap_h) * 4);
+  if (evicted) p->d2h(evicted, p->d.res_evicted, (size_t)std::min(ne, cap_ev) * 8);
+  if (inv_off && cap_ev >= ne) p->d2h(inv_off, p->d.res_inv_off, (size_t)(ne + 1) * 4);
+  const size_t n = (size_t)std::min(np, cap_pages);
+  if (pages) p->d2h(pages, p->d.res_pages, n * 8);
+  if (phys) p->d2h(phys, p->d.res_phys, n * 4);
+  if (blk) p->d2h(blk, p->d.res_blk, n * 4);
+  ck(cudaStreamSynchronize(p->stream), "apply results");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* valve_last_error(void) { return g_err.c_str(); }
+int64_t valve_kernel_launches(void) { return g_launches.load(); }
+
+void valve_pool_config_default(valve_pool_config* c) {
+  std::memset(c, 0, sizeof *c);
+  c->device = 0;
+  c->total_handles = 128;
+  c->handle_size_pages = 64;
+  c->page_size_tokens = 16;
+  c->max_requests = 4096;
+  c->max_pages_per_request = 4096;
+}
+
+int valve_pool_create_ex(const valve_pool_config* cfg, valve_pool** out) {
+  return guard([&] {
+    auto* p = new valve_pool;
+    try {
+      pool_init(p, *cfg);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+int valve_pool_create(int H, int S, int T, valve_pool** out) {
+  valve_pool_config c;
+  valve_pool_config_default(&c);
+  c.total_handles = H;
+  c.handle_size_pages = S;
+  c.page_size_tokens = T;
+  if (H > 0 && S > 0) c.max_pages_per_request = std::min<int64_t>((int64_t)H * S, 4096);
+  return valve_pool_create_ex(&c, out);
+}
+
+void valve_pool_destroy(valve_pool* p) { delete p; }
+
+int valve_pool_counts(const valve_pool* p, int64_t out[5]) {
+  p->counts(out);
+  return VALVE_OK;
+}
+
+int valve_pool_geometry(const valve_pool* p, int out[4]) {
+  out[0] = p->H;
+  out[1] = p->S;
+  out[2] = p->cfg.page_size_tokens;
+  out[3] = p->d.quarantine;
+  return VALVE_OK;
+}
+
+int64_t valve_pool_quarantine_page_id(const valve_pool* p) { return (int64_t)p->H * p->S; }
+
+int valve_pool_online_grow(valve_pool* p, int k, int64_t t) {
+  return guard([&] {
+    if (k < 0) fail(VALVE_INVALID_ARGUMENT, "online_grow: k must be >= 0");  // memory.cpp:32
+    p->launch1("online_grow", k_online_grow, 0, p->d, k, t);
+  });
+}
+
+int valve_pool_online_release(valve_pool* p, int k, int* released) {
+  return guard([&] {
+    if (k < 0) fail(VALVE_INVALID_ARGUMENT, "online_release: k must be >= 0");  // memory.cpp:38
+    p->launch1("online_release", k_online_release, 0, p->d, k, p->online_used);
+    *released = (int)p->mirror->r[0];
+  });
+}
+
+int valve_pool_online_use_pages(valve_pool* p, int64_t n) {
+  return guard([&] {
+    // memory.cpp:53-58: aggregate accounting against the device-resident capacity
+    if (n < 0) fail(VALVE_INVALID_ARGUMENT, "online_use_pages: n must be >= 0");
+    if (p->online_used + n > (int64_t)p->mirror->n_online * p->S)
+      fail(VALVE_LOGIC_ERROR, "online_use_pages: overcommit beyond reserved capacity");
+    p->online_used += n;
+  });
+}
+
+int valve_pool_online_free_pages(valve_pool* p, int64_t n) {
+  return guard([&] {
+    if (n < 0 || n > p->online_used) fail(VALVE_LOGIC_ERROR, "online_free_pages: bad page count");
+    p->online_used -= n;
+  });
+}
+
+int valve_pool_offline_reserve(valve_pool* p, int64_t req, int pages, int64_t t, int max_off, int* ok) {
+  return guard([&] {
+    if (pages < 0) fail(VALVE_INVALID_ARGUMENT, "offline_reserve: pages must be >= 0");  // memory.cpp:67
+    if (pages == 0) {  // memory.cpp:68
+      *ok = 1;
+      return;
+    }
+    p->launch1("offline_reserve", k_offline_reserve, 0, p->d, req, pages, t, max_off);
+    *ok = (int)p->mirror->r[0];
+  });
+}
+
+int valve_pool_offline_release(valve_pool* p, int64_t req) {
+  return guard([&] { p->launch1("offline_release", k_offline_release, 0, p->d, req); });
+}
+
+int valve_pool_requests_on_handle(const valve_pool* cp, int h, int64_t* out, int cap, int* n) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] {
+    if (h < 0 || h >= p->H) fail(VALVE_OUT_OF_RANGE, "requests_on_handle: handle out of range");
+    p->launch1("requests_on_handle", k_requests_on_handle, 0, p->d, h, (int64_t*)p->d.res_pages);
+    *n = (int)p->mirror->r[0];
+    if (out) p->d2h(out, p->d.res_pages, (size_t)std::min(*n, cap) * 8);
+    ck(cudaStreamSynchronize(p->stream), "requests_on_handle");
+  });
+}
+
+int valve_pool_handles_of_request(const valve_pool* cp, int64_t req, int* out, int cap, int* n) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] {
+    p->launch1("handles_of_request", k_handles_of_request, 0, p->d, req, p->d.res_handles);
+    *n = (int)p->mirror->r[0];
+    if (out) p->d2h(out, p->d.res_handles, (size_t)std::min(*n, cap) * 4);
+    ck(cudaStreamSynchronize(p->stream), "handles_of_request");
+  });
+}
+
+int valve_pool_offline_pages_of(const valve_pool* cp, int64_t req, int* out) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] {
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    k_offline_pages_of<<<1, 32, 0, p->stream>>>(p->d, req);
+    counted();
+    p->sync_and_check("offline_pages_of");
+    *out = (int)p->mirror->r[0];
+  });
+}
+
+int valve_pool_request_row(const valve_pool* cp, int64_t req, int* row) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] {
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    k_offline_pages_of<<<1, 32, 0, p->stream>>>(p->d, req);
+    counted();
+    p->sync_and_check("request_row");
+    *row = (int)p->mirror->r[1];
+  });
+}
+
+int valve_pool_block_table(const valve_pool* cp, int64_t req, int* out, int cap, int* n) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] {
+    p->launch1("block_table", k_block_table, 0, p->d, req, p->d.res_phys);
+    *n = (int)p->mirror->r[0];
+    if (out) p->d2h(out, p->d.res_phys, (size_t)std::min(*n, cap) * 4);
+    ck(cudaStreamSynchronize(p->stream), "block_table");
+  });
+}
+
+int valve_pool_snapshot(const valve_pool* cp, int* ids, int64_t* mapped, int* off, int64_t* reqs,
+                        int cap_h, int cap_r, int* nh, int* nr) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] {
+    p->launch1("snapshot", k_snapshot, p->smem_snapshot, p->d);
+    *nh = (int)p->mirror->r[0];
+    *nr = (int)p->mirror->r[1];
+    if (ids) p->d2h(ids, p->d.s_hid, (size_t)std::min(*nh, cap_h) * 4);
+    if (mapped) p->d2h(mapped, p->d.s_hmap, (size_t)std::min(*nh, cap_h) * 8);
+    if (off && cap_h >= *nh) p->d2h(off, p->d.s_roff, (size_t)(*nh + 1) * 4);
+    if (reqs) p->d2h(reqs, p->d.res_pages, (size_t)std::min(*nr, cap_r) * 8);
+    ck(cudaStreamSynchronize(p->stream), "snapshot");
+  });
+}
+
+int valve_pool_apply_reclaim(valve_pool* p, const int* ids, int k, int64_t t, int* handles,
+                             int* n_handles, int64_t* evicted, int* n_evicted, int* inv_off,
+                             int64_t* inv_pages, int* inv_phys, int* inv_blk, int cap_ev,
+                             int cap_pages, int* n_pages) {
+  int code = guard([&] {
+    if (k < 0) fail(VALVE_INVALID_ARGUMENT, "apply_reclaim: negative handle count");
+    // beyond H+1 entries the list must already contain a repeat or a bad id, at which the
+    // reference stops (memory.cpp:160-161): only that prefix matters
+    k = std::min(k, p->H + 1);
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    if (k) ck(cudaMemcpyAsync(p->d_ids, ids, (size_t)k * 4, cudaMemcpyHostToDevice, p->stream), "upload ids");
+    try {
+      p->launch1("apply_reclaim", k_apply, 0, p->d, (const int*)p->d_ids, k, t);
+    } catch (const Err&) {
+      p->last_n_handles = (int)p->mirror->r[0];
+      p->last_n_evicted = (int)p->mirror->r[1];
+      p->last_n_pages = (int)p->mirror->r[2];
+      throw;
+    }
+    p->last_n_handles = (int)p->mirror->r[0];
+    p->last_n_evicted = (int)p->mirror->r[1];
+    p->last_n_pages = (int)p->mirror->r[2];
+  });
+  if (n_handles) *n_handles = p->last_n_handles;
+  if (n_evicted) *n_evicted = p->last_n_evicted;
+  if (n_pages) *n_pages = p->last_n_pages;
+  if (code != VALVE_OK && code != VALVE_LOGIC_ERROR && code != VALVE_OUT_OF_RANGE) return code;
+  const std::string saved = g_err;
+  const int rc = guard([&] {
+    read_apply_results(p, handles, evicted, inv_off, inv_pages, inv_phys, inv_blk, p->H, cap_ev,
+                       cap_pages);
+  });
+  if (code != VALVE_OK) {
+    g_err = saved;
+    return code;
+  }
+  return rc;
+}
+
+int valve_pool_handle_state(const valve_pool* cp, int h, int* st) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] {
+    if (h < 0 || h >= p->H) fail(VALVE_OUT_OF_RANGE, "handle_state: handle out of range");
+    uint8_t v = 0;
+    ck(cudaMemcpyAsync(&v, p->d.hstate + h, 1, cudaMemcpyDeviceToHost, p->stream), "read");
+    ck(cudaStreamSynchronize(p->stream), "read");
+    *st = v;
+  });
+}
+
+int valve_pool_handle_mapped_at(const valve_pool* cp, int h, int64_t* t) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] {
+    if (h < 0 || h >= p->H) fail(VALVE_OUT_OF_RANGE, "handle_mapped_at: handle out of range");
+    ck(cudaMemcpyAsync(t, p->d.hmapped + h, 8, cudaMemcpyDeviceToHost, p->stream), "read");
+    ck(cudaStreamSynchronize(p->stream), "read");
+  });
+}
+
+int valve_pool_check_invariants(const valve_pool* cp) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] { p->launch1("check_invariants", k_check_invariants, 0, p->d, p->online_used); });
+}
+
+int valve_pool_set_costs(valve_pool* p, int n, const int64_t* reqs, const int64_t* costs) {
+  return guard([&] {
+    if (n < 0 || n > p->R) fail(VALVE_INVALID_ARGUMENT, "set_costs: bad count");
+    if (!n) return;
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    ck(cudaMemcpyAsync(p->d_in64, reqs, (size_t)n * 8, cudaMemcpyHostToDevice, p->stream), "upload");
+    ck(cudaMemcpyAsync(p->d_in64b, costs, (size_t)n * 8, cudaMemcpyHostToDevice, p->stream), "upload");
+    p->launch1("set_costs", k_set_costs, 0, p->d, n, (const int64_t*)p->d_in64,
+               (const int64_t*)p->d_in64b);
+    if (p->mirror->r[0]) fail(VALVE_INVALID_ARGUMENT, "set_costs: request has no live pages in the pool");
+  });
+}
+
+int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles, int* n_evicted,
+                       int* n_pages) {
+  return guard([&] {
+    if (k < 0) fail(VALVE_INVALID_ARGUMENT, "selective_reclaim: k must be >= 0");
+    if (mode != VALVE_SELECT_SELECTIVE && mode != VALVE_SELECT_FIFO)
+      fail(VALVE_INVALID_ARGUMENT, "reclaim: device-fused mode must be selective or fifo");
+    p->launch1("reclaim", k_reclaim, p->smem_reclaim, p->d, k, mode, t);
+    p->last_n_handles = (int)p->mirror->r[0];
+    p->last_n_evicted = (int)p->mirror->r[1];
+    p->last_n_pages = (int)p->mirror->r[2];
+    if (n_handles) *n_handles = p->last_n_handles;
+    if (n_evicted) *n_evicted = p->last_n_evicted;
+    if (n_pages) *n_pages = p->last_n_pages;
+  });
+}
+
+int valve_pool_last_reclaim(const valve_pool* cp, int* handles, int64_t* evicted, int* inv_off,
+                            int64_t* inv_pages, int* inv_phys, int* inv_blk, int cap_h, int cap_ev,
+                            int cap_pages) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] {
+    read_apply_results(p, handles, evicted, inv_off, inv_pages, inv_phys, inv_blk, cap_h, cap_ev,
+                       cap_pages);
+  });
+}
+
+int valve_pool_fill_pages(valve_pool* p) {
+  return guard([&] {
+    if (!p->d.pages) fail(VALVE_LOGIC_ERROR, "fill_pages: pool has no page store (slot_bytes = 0)");
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    k_fill_pages<<<148 * 8, 256, 0, p->stream>>>(p->d);
+    counted();
+    p->sync_and_check("fill_pages");
+  });
+}
+
+int valve_pool_view_get(const valve_pool* p, valve_pool_view* v) {
+  v->pages = p->d.pages;
+  v->block_tables = p->d.bt;
+  v->slot_bytes = p->d.slot_bytes;
+  v->page_bytes = p->d.page_bytes;
+  v->max_pages_per_request = p->Pblk;
+  v->quarantine_page = p->d.quarantine;
+  v->stream = p->stream;
+  return VALVE_OK;
+}
+
+// -------------------------------------------------------------------------- reclaim copy
+
+void valve_copy_params_default(valve_copy_params* c) {
+  c->ctas = 16;
+  c->threads = 512;
+  c->chunk_bytes = 65536;
+  c->rate_bytes_per_s = 0;
+  c->burst_bytes = 0;
+  c->use_tma = 0;
+}
+
+int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
+                            const valve_copy_params* prm, valve_copy_stats* st) {
+  return guard([&] {
+    valve_copy_params c;
+    valve_copy_params_default(&c);
+    if (prm) c = *prm;
+    if (c.ctas <= 0) c.ctas = 16;
+    if (c.threads <= 0) c.threads = 512;
+    if (c.chunk_bytes <= 0) c.chunk_bytes = 65536;
+    if (!p->d.pages) fail(VALVE_LOGIC_ERROR, "reclaim_copy: pool has no page store");
+    if (c.chunk_bytes % 16 || c.threads % 32 || c.threads > 512)
+      fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: chunk must be a 16-byte multiple, threads <= 512");
+    const int64_t need = (int64_t)p->last_n_pages * p->d.page_bytes;
+    if (dst_bytes < need) fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: destination too small");
+    if (reinterpret_cast<uintptr_t>(host_dst) % 16)
+      fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: destination must be 16-byte aligned");
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    void* ddst = nullptr;
+    ck(cudaHostGetDevicePointer(&ddst, host_dst, 0),
+       "reclaim_copy: destination is not pinned/mapped host memory");
+    CopyArgs A{};
+    A.pages = p->d.pages;
+    A.slot_bytes = p->d.slot_bytes;
+    A.page_bytes = p->d.page_bytes;
+    A.chunk_bytes = c.chunk_bytes;
+    A.phys = p->d.res_phys;
+    A.n_pages = p->last_n_pages;
+    const int64_t cpp = (A.page_bytes + c.chunk_bytes - 1) / c.chunk_bytes;
+    A.n_chunks = (int64_t)A.n_pages * cpp;
+    A.dst = static_cast<uint8_t*>(ddst);
+    A.ns_per_byte = c.rate_bytes_per_s > 0 ? 1e9 / c.rate_bytes_per_s : 0.0;
+    A.burst_bytes = c.burst_bytes;
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(p->d_in64);  // 3 words
+    ck(cudaMemsetAsync(ctr, 0, 24, p->stream), "memset");
+    A.cursor = ctr;
+    A.t_first = ctr + 1;
+    A.t_last = ctr + 2;
+    ck(cudaEventRecord(p->ev0, p->stream), "event");
+    if (A.n_chunks > 0) {
+      if (c.use_tma) {
+        static bool attr = false;
+        if (!attr) {
+          ck(cudaFuncSetAttribute(k_reclaim_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  2 * 32768),
+             "cudaFuncSetAttribute");
+          attr = true;
+        }
+        k_reclaim_copy_tma<<<c.ctas, 32, 2 * 32768, p->stream>>>(A);
+      } else {
+        k_reclaim_copy<<<c.ctas, c.threads, 0, p->stream>>>(A);
+      }
+      counted();
+    }
+    ck(cudaEventRecord(p->ev1, p->stream), "event");
+    ck(cudaGetLastError(), "reclaim_copy launch");
+    ck(cudaStreamSynchronize(p->stream), "reclaim_copy");
+    if (st) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, p->ev0, p->ev1), "event");
+      unsigned long long t[3];
+      ck(cudaMemcpy(t, ctr, 24, cudaMemcpyDeviceToHost), "read");
+      st->bytes = need;
+      st->pages = p->last_n_pages;
+      st->kernel_ms = ms;
+      st->t_first_ns = t[1];
+      st->t_last_ns = t[2];
+    }
+  });
+}
+
+int valve_host_alloc(int64_t bytes, void** out) {
+  return guard([&] {
+    if (bytes <= 0) fail(VALVE_INVALID_ARGUMENT, "host_alloc: bytes must be > 0");
+    ck(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc");
+  });
+}
+
+void valve_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int valve_pool_reclaim_copy_ce(valve_pool* p, void* host_dst, int64_t dst_bytes, valve_copy_stats* st) {
+  return guard([&] {
+    if (!p->d.pages) fail(VALVE_LOGIC_ERROR, "reclaim_copy: pool has no page store");
+    const int64_t need = (int64_t)p->last_n_pages * p->d.page_bytes;
+    if (dst_bytes < need) fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: destination too small");
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    std::vector<int> phys(p->last_n_pages);
+    if (!phys.empty()) {
+      ck(cudaMemcpyAsync(phys.data(), p->d.res_phys, phys.size() * 4, cudaMemcpyDeviceToHost, p->stream), "read");
+      ck(cudaStreamSynchronize(p->stream), "read");
+    }
+    ck(cudaEventRecord(p->ev0, p->stream), "event");
+    for (size_t i = 0; i < phys.size(); ++i)
+      ck(cudaMemcpyAsync(static_cast<uint8_t*>(host_dst) + i * p->d.page_bytes,
+                         p->d.pages + (int64_t)phys[i] * p->d.slot_bytes, (size_t)p->d.page_bytes,
+                         cudaMemcpyDeviceToHost, p->stream),
+         "cudaMemcpyAsync");
+    ck(cudaEventRecord(p->ev1, p->stream), "event");
+    ck(cudaStreamSynchronize(p->stream), "reclaim_copy_ce");
+    if (st) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, p->ev0, p->ev1), "event");
+      st->bytes = need;
+      st->pages = p->last_n_pages;
+      st->kernel_ms = ms;
+      st->t_first_ns = st->t_last_ns = 0;
+    }
+  });
+}
+
+}  // extern "C"
+
+// =================================================================== selection (host instance)
+
+namespace {
+
+struct SelectCtx {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  int64_t cap_n = 0, cap_nnz = 0, cap_m = 0;
+  int* hid = nullptr;
+  int64_t* mapped = nullptr;
+  int* roff = nullptr;
+  int64_t* reqs = nullptr;
+  int* rref = nullptr;
+  int64_t* keys = nullptr;
+  int64_t* cost = nullptr;
+  int64_t* marg = nullptr;
+  int* taken = nullptr;
+  int* ev = nullptr;
+  int* qoff = nullptr;
+  int* qcnt = nullptr;
+  int* qh = nullptr;
+  int* out = nullptr;
+  int* pick = nullptr;
+  int* status = nullptr;
+  int64_t* result = nullptr;
+  std::mutex mu;
+
+  template <class T>
+  void grow(T*& ptr, int64_t n) {
+    if (ptr) cudaFree(ptr);
+    ck(cudaMalloc((void**)&ptr, std::max<int64_t>(n, 1) * sizeof(T)), "cudaMalloc");
+  }
+  void reserve(int64_t n, int64_t nnz, int64_t m) {
+    if (!stream) ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+    if (!status) {
+      grow(status, 4);
+      grow(result, 2);
+    }
+    if (n > cap_n) {
+      cap_n = std::max<int64_t>(n, 2 * cap_n);
+      grow(hid, cap_n);
+      grow(mapped, cap_n);
+      grow(roff, cap_n + 1);
+      grow(marg, cap_n);
+      grow(taken, cap_n);
+      grow(out, cap_n);
+      grow(pick, cap_n);
+    }
+    if (nnz > cap_nnz) {
+      cap_nnz = std::max<int64_t>(nnz, 2 * cap_nnz);
+      grow(reqs, cap_nnz);
+      grow(rref, cap_nnz);
+      grow(qh, cap_nnz);
+    }
+    const int64_t mm = std::max(m, n);
+    if (mm > cap_m) {
+      cap_m = std::max<int64_t>(mm, 2 * cap_m);
+      grow(keys, cap_m);
+      grow(cost, cap_m);
+      grow(ev, cap_m);
+      grow(qoff, cap_m + 1);
+      grow(qcnt, std::max(cap_m, cap_n));
+    }
+  }
+};
+
+SelectCtx& select_ctx(int device) {
+  static SelectCtx ctx[16];
+  if (device < 0 || device >= 16) fail(VALVE_INVALID_ARGUMENT, "select: bad device ordinal");
+  ctx[device].device = device;
+  return ctx[device];
+}
+
+SelectArgs upload_instance(SelectCtx& C, int n, const int* ids, const int64_t* mapped, const int* off,
+                           const int64_t* reqs, int m, const int64_t* keys, const int64_t* vals, int k,
+                           int mode) {
+  const int nnz = n ? off[n] : 0;
+  C.reserve(n, nnz, m);
+  auto up = [&](void* d, const void* h, size_t b) {
+    if (b) ck(cudaMemcpyAsync(d, h, b, cudaMemcpyHostToDevice, C.stream), "upload");
+  };
+  up(C.hid, ids, (size_t)n * 4);
+  if (mapped) up(C.mapped, mapped, (size_t)n * 8);
+  up(C.roff, off, (size_t)(n + 1) * 4);
+  up(C.reqs, reqs, (size_t)nnz * 8);
+  up(C.keys, keys, (size_t)m * 8);
+  up(C.cost, vals, (size_t)m * 8);
+  if (nnz) {
+    k_map_refs<<<(nnz + 255) / 256, 256, 0, C.stream>>>(C.reqs, nnz, C.keys, m, C.rref);
+    counted();
+  }
+  SelectArgs A{};
+  A.n = n;
+  A.m = m;
+  A.k = k;
+  A.mode = mode;
+  A.nnz = nnz;
+  A.hid = C.hid;
+  A.mapped = C.mapped;
+  A.roff = C.roff;
+  A.rref = C.rref;
+  A.cost = C.cost;
+  A.marg = C.marg;
+  A.taken = C.taken;
+  A.ev = C.ev;
+  A.qoff = C.qoff;
+  A.qcnt = C.qcnt;
+  A.qh = C.qh;
+  A.out = C.out;
+  A.status = C.status;
+  A.result = C.result;
+  return A;
+}
+
+}  // namespace
+
+extern "C" {
+
+int valve_select(int device, int n, const int* ids, const int64_t* mapped, const int* off,
+                 const int64_t* reqs, int m, const int64_t* keys, const int64_t* vals, int k, int mode,
+                 int* out, int* n_out) {
+  return guard([&] {
+    const char* who = mode == 0 ? "selective_reclaim" : mode == 1 ? "fifo_reclaim" : "oracle_reclaim";
+    if (mode < 0 || mode > 2) fail(VALVE_INVALID_ARGUMENT, "select: unknown mode");
+    if (k < 0) fail(VALVE_INVALID_ARGUMENT, std::string(who) + ": k must be >= 0");  // reclaim.cpp:34,70,86
+    if (mode == 2 && n > 20)
+      fail(VALVE_INVALID_ARGUMENT, "oracle_reclaim: instance too large (> 20 handles)");  // reclaim.cpp:88
+    if (n < 0 || m < 0) fail(VALVE_INVALID_ARGUMENT, "select: negative sizes");
+    k = std::min(k, n);
+    *n_out = k;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0)
+      fail(VALVE_CUDA_ERROR, "no CUDA device: selection runs only on the GPU");
+    SelectCtx& C = select_ctx(device);
+    std::lock_guard<std::mutex> lk(C.mu);
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    SelectArgs A = upload_instance(C, n, ids, mapped, off, reqs, m, keys, vals, k, mode);
+    k_select_instance<<<1, kNT, 0, C.stream>>>(A);
+    counted();
+    ck(cudaGetLastError(), "select launch");
+    int status = 0;
+    ck(cudaMemcpyAsync(&status, C.status, 4, cudaMemcpyDeviceToHost, C.stream), "read");
+    if (k) ck(cudaMemcpyAsync(out, C.out, (size_t)k * 4, cudaMemcpyDeviceToHost, C.stream), "read");
+    ck(cudaStreamSynchronize(C.stream), "select");
+    if (status == kDetNoCost) fail(VALVE_INVALID_ARGUMENT, "reclaim: request without cost entry");
+  });
+}
+
+int valve_evicted_cost(int device, int n, const int* ids, const int* off, const int64_t* reqs, int m,
+                       const int64_t* keys, const int64_t* vals, const int* pick, int n_pick,
+                       int64_t* cost) {
+  return guard([&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0)
+      fail(VALVE_CUDA_ERROR, "no CUDA device: evicted_cost runs only on the GPU");
+    SelectCtx& C = select_ctx(device);
+    std::lock_guard<std::mutex> lk(C.mu);
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    SelectArgs A = upload_instance(C, n, ids, nullptr, off, reqs, m, keys, vals, 0, 0);
+    C.reserve(n, n ? off[n] : 0, std::max(m, n_pick));
+    if (n_pick > C.cap_n) C.reserve(n_pick, 0, 0);
+    if (n_pick)
+      ck(cudaMemcpyAsync(C.pick, pick, (size_t)n_pick * 4, cudaMemcpyHostToDevice, C.stream), "upload");
+    A.ev = C.ev;
+    k_evicted_cost<<<1, 32, 0, C.stream>>>(A, C.pick, n_pick);
+    counted();
+    ck(cudaGetLastError(), "evicted_cost launch");
+    int status = 0;
+    ck(cudaMemcpyAsync(&status, C.status, 4, cudaMemcpyDeviceToHost, C.stream), "read");
+    ck(cudaMemcpyAsync(cost, C.result, 8, cudaMemcpyDeviceToHost, C.stream), "read");
+    ck(cudaStreamSynchronize(C.stream), "evicted_cost");
+    if (status == kDetApplyRange) fail(VALVE_INVALID_ARGUMENT, "evicted_cost: unknown handle id");
+    if (status == kDetNoCost) fail(VALVE_INVALID_ARGUMENT, "reclaim: request without cost entry");
+  });
+}
+
+// =============================================================== reservation controller
+
+}  // extern "C"
+
+struct valve_resctl {
+  valve_resparams p;
+  int64_t t = 0, last_tick = 0;
+  std::vector<int64_t> pressure;  // event times, ascending (record order)
+};
+
+extern "C" {
+
+void valve_resparams_default(valve_resparams* p) {
+  // memory.hpp:103-114
+  p->alpha = 1.5;
+  p->beta = 2.0;
+  p->t_init_us = 1000000;
+  p->delta_us = 100000;
+  p->t_min_us = 100000;
+  p->t_max_us = 60000000;
+  p->window_us = 60000000;
+  p->target_per_window = 1.0;
+  p->h_min = 1;
+  p->pressure_threshold = 0.9;
+}
+
+int valve_resctl_create(const valve_resparams* p, valve_resctl** out) {
+  return guard([&] {
+    // memory.cpp:213-218
+    if (p->alpha <= 1.0 || p->beta <= 1.0)
+      fail(VALVE_INVALID_ARGUMENT, "ReservationParams: alpha/beta must be > 1");
+    if (p->t_init_us <= 0 || p->t_min_us <= 0 || p->t_max_us < p->t_min_us || p->window_us <= 0)
+      fail(VALVE_INVALID_ARGUMENT, "ReservationParams: bad interval bounds");
+    if (p->h_min < 0) fail(VALVE_INVALID_ARGUMENT, "ReservationParams: h_min must be >= 0");
+    auto* c = new valve_resctl;
+    c->p = *p;
+    c->t = p->t_init_us;
+    *out = c;
+  });
+}
+void valve_resctl_destroy(valve_resctl* c) { delete c; }
+int64_t valve_resctl_interval(const valve_resctl* c) { return c->t; }
+int64_t valve_resctl_pressure_events(const valve_resctl* c) { return (int64_t)c->pressure.size(); }
+int valve_resctl_grow_target(const valve_resctl* c, int h, int cap) {
+  // memory.cpp:220-223 -- IEEE-double ceil, then clamps
+  const int target = (int)std::ceil(c->p.alpha * (double)h);
+  return std::min(std::max({target, h, 1}), cap);
+}
+void valve_resctl_record_pressure(valve_resctl* c, int64_t t) { c->pressure.push_back(t); }
+int valve_resctl_release_due(const valve_resctl* c, int64_t t, int h) {
+  // memory.cpp:227-234: quiet since the previous tick?
+  if (h <= c->p.h_min) return 0;
+  for (auto it = c->pressure.rbegin(); it != c->pressure.rend() && *it > c->last_tick; ++it)
+    if (*it <= t) return 0;
+  return 1;
+}
+void valve_resctl_note_tick(valve_resctl* c, int64_t t) { c->last_tick = t; }
+int64_t valve_resctl_pressure_in_window(const valve_resctl* c, int64_t t) {
+  // memory.cpp:248-255: events in (t - window, t]
+  int64_t n = 0;
+  for (auto it = c->pressure.rbegin(); it != c->pressure.rend() && *it > t - c->p.window_us; ++it)
+    n += *it <= t;
+  return n;
+}
+int64_t valve_resctl_window_tick(valve_resctl* c, int64_t t) {
+  // memory.cpp:238-246: x beta (truncated double) on a hot window, - delta otherwise
+  const double rate = (double)valve_resctl_pressure_in_window(c, t);
+  if (rate > c->p.target_per_window)
+    c->t = std::min((int64_t)((double)c->t * c->p.beta), c->p.t_max_us);
+  else
+    c->t = std::max(c->t - c->p.delta_us, c->p.t_min_us);
+  return c->t;
+}
+
+}  // extern "C"
+
+// ================================================================================= gate
+
+struct valve_gate {
+  int device = 0;
+  GateDev* d = nullptr;
+  cudaStream_t stream = nullptr;  // high priority
+  std::vector<valve_gate*> peers;
+  int64_t* d_prefix = nullptr;
+  int64_t cap_prefix = 0;
+  ~valve_gate() {
+    if (stream) cudaStreamSynchronize(stream);
+    if (d) cudaFree(d);
+    if (d_prefix) cudaFree(d_prefix);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+cudaStream_t as_stream(void* s, cudaStream_t dflt) { return s ? static_cast<cudaStream_t>(s) : dflt; }
+CUdeviceptr dptr(const void* p) { return reinterpret_cast<CUdeviceptr>(p); }
+}  // namespace
+
+extern "C" {
+
+int valve_gate_create(int device, valve_gate** out) {
+  return guard([&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0)
+      fail(VALVE_CUDA_ERROR, "no CUDA device: the gate lives in HBM");
+    memops();
+    auto* g = new valve_gate;
+    g->device = device;
+    try {
+      ck(cudaSetDevice(device), "cudaSetDevice");
+      int lo = 0, hi = 0;
+      ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+      ck(cudaStreamCreateWithPriority(&g->stream, cudaStreamNonBlocking, hi), "stream");
+      ck(cudaMalloc((void**)&g->d, sizeof(GateDev)), "cudaMalloc");
+      ck(cudaMemset(g->d, 0, sizeof(GateDev)), "memset");
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+void valve_gate_destroy(valve_gate* g) { delete g; }
+
+void* valve_gate_stream(const valve_gate* g) { return g->stream; }
+
+int valve_gate_raise(valve_gate* g, uint32_t gen, void* s) {
+  return guard([&] {
+    const MemOps& op = memops();
+    cudaStream_t st = as_stream(s, g->stream);
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    // leader first, then the TP members' words over peer memory (flat fan-out)
+    std::vector<valve_gate*> all{g};
+    all.insert(all.end(), g->peers.begin(), g->peers.end());
+    for (valve_gate* x : all) {
+      cu_ck(op.write64((CUstream)st, dptr(&x->d->t_first_seen), 0, 0), "cuStreamWriteValue64");
+      cu_ck(op.write32((CUstream)st, dptr(&x->d->gen), gen, 0), "cuStreamWriteValue32");
+      cu_ck(op.write32((CUstream)st, dptr(&x->d->closed), 1, 0), "cuStreamWriteValue32");
+    }
+  });
+}
+
+int valve_gate_release(valve_gate* g, uint32_t gen, void* s) {
+  return guard([&] {
+    const MemOps& op = memops();
+    cudaStream_t st = as_stream(s, g->stream);
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    std::vector<valve_gate*> all{g};
+    all.insert(all.end(), g->peers.begin(), g->peers.end());
+    for (valve_gate* x : all) {
+      cu_ck(op.write32((CUstream)st, dptr(&x->d->gen), gen, 0), "cuStreamWriteValue32");
+      cu_ck(op.write32((CUstream)st, dptr(&x->d->closed), 0, 0), "cuStreamWriteValue32");
+    }
+  });
+}
+
+int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* s) {
+  return guard([&] {
+    const MemOps& op = memops();
+    cudaStream_t st = as_stream(s, g->stream);
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    std::vector<valve_gate*> all{g};
+    all.insert(all.end(), g->peers.begin(), g->peers.end());
+    for (valve_gate* x : all) {
+      cu_ck(op.wait32((CUstream)st, dptr(&x->d->live_ctas), 0, CU_STREAM_WAIT_VALUE_EQ),
+            "cuStreamWaitValue32");
+      cu_ck(op.write32((CUstream)st, dptr(&x->d->quiesced_gen), gen, 0), "cuStreamWriteValue32");
+    }
+  });
+}
+
+int valve_gate_attach_peers(valve_gate* leader, valve_gate** members, int n) {
+  return guard([&] {
+    ck(cudaSetDevice(leader->device), "cudaSetDevice");
+    for (int i = 0; i < n; ++i) {
+      valve_gate* m = members[i];
+      if (m->device != leader->device) {
+        int ok = 0;
+        ck(cudaDeviceCanAccessPeer(&ok, leader->device, m->device), "cudaDeviceCanAccessPeer");
+        if (!ok) fail(VALVE_RUNTIME_ERROR, "attach_peers: no peer access between the GPUs");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(m->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "cudaDeviceEnablePeerAccess");
+        cudaGetLastError();
+      }
+      leader->peers.push_back(m);
+    }
+  });
+}
+
+int valve_gate_read(const valve_gate* g, valve_gate_state* o) {
+  return guard([&] {
+    GateDev h{};
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    ck(cudaMemcpy(&h, g->d, sizeof h, cudaMemcpyDeviceToHost), "read gate");
+    o->gen = h.gen;
+    o->closed = h.closed;
+    o->quiesced_gen = h.quiesced_gen;
+    o->live_ctas = h.live_ctas;
+    o->t_first_seen_ns = h.t_first_seen;
+    o->t_quiesced_ns = h.t_quiesced;
+    o->tiles_done = h.tiles_done;
+    o->canary_hits = h.canary;
+    o->tiles_claimed = h.cursor;
+  });
+}
+
+int valve_offline_reset(valve_gate* g) {
+  return guard([&] {
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    ck(cudaMemsetAsync(&g->d->cursor, 0, 3 * sizeof(unsigned long long), g->stream), "memset");
+    ck(cudaMemsetAsync(&g->d->t_first_seen, 0, 2 * sizeof(unsigned long long), g->stream), "memset");
+    ck(cudaStreamSynchronize(g->stream), "reset");
+  });
+}
+
+int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work* w, void* s) {
+  return guard([&] {
+    const MemOps& op = memops();
+    if (!p->d.pages) fail(VALVE_LOGIC_ERROR, "offline_launch: pool has no page store");
+    if (w->n_requests <= 0) return;
+    cudaStream_t st = as_stream(s, p->stream);
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    const int64_t chunk = 65536;
+    const int cpp = (int)((p->d.page_bytes + chunk - 1) / chunk);
+    if (w->n_requests + 1 > g->cap_prefix) {
+      if (g->d_prefix) cudaFree(g->d_prefix);
+      g->cap_prefix = std::max<int64_t>(w->n_requests + 1, 2 * g->cap_prefix);
+      ck(cudaMalloc((void**)&g->d_prefix, g->cap_prefix * 8), "cudaMalloc");
+    }
+    k_tile_prefix<<<1, kNT, 0, st>>>(w->npages, w->n_requests, cpp, g->d_prefix);
+    counted();
+    int threads = w->threads > 0 ? w->threads : 256;
+    int ctas = w->ctas;
+    if (ctas <= 0) {
+      int per_sm = 0, sms = 0;
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_offline_decode, threads, 0), "occupancy");
+      ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device), "attr");
+      ctas = per_sm * sms;
+    }
+    // never start tiles into a closed gate; count the CTAs before they can retire
+    cu_ck(op.wait32((CUstream)st, dptr(&g->d->closed), 0, CU_STREAM_WAIT_VALUE_EQ), "cuStreamWaitValue32");
+    cu_ck(op.write32((CUstream)st, dptr(&g->d->live_ctas), (cuuint32_t)ctas, 0), "cuStreamWriteValue32");
+    OfflineArgs A{};
+    A.g = g->d;
+    A.pages = p->d.pages;
+    A.slot_bytes = p->d.slot_bytes;
+    A.page_bytes = p->d.page_bytes;
+    A.chunk_bytes = chunk;
+    A.chunks_per_page = cpp;
+    A.bt = p->d.bt;
+    A.P = p->Pblk;
+    A.quarantine = p->d.quarantine;
+    A.rows = w->rows;
+    A.tile_prefix = g->d_prefix;
+    A.n_requests = w->n_requests;
+    A.total_tiles = w->total_tiles;
+    A.out = w->out;
+    A.poll = w->poll;
+    k_offline_decode<<<ctas, threads, 0, st>>>(A);
+    counted();
+    ck(cudaGetLastError(), "offline launch");
+  });
+}
+
+}  // extern "C"
+
+// ============================================================================= channel
+
+struct valve_channel {
+  // channel.hpp:69-79
+  int64_t toggle = 0, cooldown = 0;
+  valve_channel_hooks h{};
+  int state = 0;  // 0 enabled, 1 disabling, 2 disabled, 3 enabling (channel.hpp:32)
+  bool any_busy = false, enable_after_disable = false, cooldown_pending = false;
+  int64_t gen = 0, cooldown_gen = 0, effective_at = 0, disables = 0;
+  valve_gate* gate = nullptr;
+
+  void log(int64_t t, int what, int64_t aux, int mem) {
+    if (h.log) h.log(h.user, t, what, aux, mem);
+  }
+  int gate_status = VALVE_OK;  // last device-gate store (the C hooks return void)
+  void gate_raise() {
+    if (gate) gate_status = valve_gate_raise(gate, (uint32_t)gen, nullptr);
+  }
+  void gate_release() {
+    if (gate) gate_status = valve_gate_release(gate, (uint32_t)gen, nullptr);
+  }
+  void issue_disable(int64_t t, bool mem) {
+    // channel.cpp:13-20; the device gate closes at issue (offline stops at its next tile)
+    state = 1;
+    effective_at = t + toggle;
+    ++gen;
+    ++disables;
+    gate_raise();
+    if (h.schedule) h.schedule(h.user, effective_at, gen, 0);
+    log(t, 0, effective_at, mem ? 1 : 0);
+  }
+  void issue_enable(int64_t t) {
+    // channel.cpp:22-28
+    state = 3;
+    effective_at = t + toggle;
+    ++gen;
+    if (h.schedule) h.schedule(h.user, effective_at, gen, 0);
+    log(t, 2, effective_at, 0);
+  }
+};
+
+extern "C" {
+
+int valve_channel_create(int64_t toggle, int64_t cooldown, const valve_channel_hooks* hooks,
+                         valve_channel** out) {
+  return guard([&] {
+    if (toggle < 0 || cooldown < 0)
+      fail(VALVE_INVALID_ARGUMENT, "ChannelController: latencies must be >= 0");  // channel.cpp:9-10
+    auto* c = new valve_channel;
+    c->toggle = toggle;
+    c->cooldown = cooldown;
+    if (hooks) c->h = *hooks;
+    *out = c;
+  });
+}
+void valve_channel_destroy(valve_channel* c) { delete c; }
+int valve_channel_bind_gate(valve_channel* c, valve_gate* g) {
+  c->gate = g;
+  return VALVE_OK;
+}
+int valve_channel_state(const valve_channel* c) { return c->state; }
+int valve_channel_offline_compute_allowed(const valve_channel* c) { return c->state == 0; }
+int64_t valve_channel_disables_issued(const valve_channel* c) { return c->disables; }
+int64_t valve_channel_pending_effective(const valve_channel* c) { return c->effective_at; }
+
+void valve_channel_note_busy(valve_channel* c, int64_t t) {
+  // channel.cpp:30-39
+  c->any_busy = true;
+  c->enable_after_disable = false;
+  if (c->cooldown_pending) {
+    c->cooldown_pending = false;
+    ++c->cooldown_gen;
+    c->log(t, 5, 0, 0);
+  }
+  if (c->state == 0 || c->state == 3) c->issue_disable(t, false);
+}
+
+void valve_channel_note_all_idle(valve_channel* c, int64_t t) {
+  // channel.cpp:41-48
+  c->any_busy = false;
+  if (c->state == 0 || c->state == 3) return;
+  c->cooldown_pending = true;
+  ++c->cooldown_gen;
+  if (c->h.schedule) c->h.schedule(c->h.user, t + c->cooldown, c->cooldown_gen, 1);
+  c->log(t, 4, t + c->cooldown, 0);
+}
+
+int64_t valve_channel_ensure_disabled(valve_channel* c, int64_t t) {
+  // channel.cpp:50-62
+  if (c->state == 2) return t;
+  if (c->state == 1) return c->effective_at;
+  c->issue_disable(t, true);
+  return c->effective_at;
+}
+
+void valve_channel_handle_toggle(valve_channel* c, int64_t t, int64_t gen) {
+  // channel.cpp:64-79
+  if (gen != c->gen) return;
+  if (c->state == 1) {
+    c->state = 2;
+    c->log(t, 1, 0, 0);
+    if (c->h.on_disabled) c->h.on_disabled(c->h.user, t);
+    if (c->enable_after_disable && !c->any_busy) {
+      c->enable_after_disable = false;
+      c->issue_enable(t);
+    }
+  } else if (c->state == 3) {
+    c->state = 0;
+    c->gate_release();  // offline may claim tiles again
+    c->log(t, 3, 0, 0);
+    if (c->h.on_enabled) c->h.on_enabled(c->h.user, t);
+  }
+}
+
+void valve_channel_handle_cooldown(valve_channel* c, int64_t t, int64_t gen) {
+  // channel.cpp:81-90
+  if (gen != c->cooldown_gen || !c->cooldown_pending) return;
+  c->cooldown_pending = false;
+  if (c->any_busy) return;
+  if (c->state == 2) c->issue_enable(t);
+  else if (c->state == 1) c->enable_after_disable = true;
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// valve_kernels.h -- kernel entry points shared between the .cu translation units.
+#pragma once
+#include "valve_common.cuh"
+
+namespace valve {
+
+// Device-side arguments of the selection kernels over a host-provided instance.
+struct SelectArgs {
+  int n, m, k, mode, nnz;
+  const int* hid;
+  const int64_t* mapped;
+  const int* roff;
+  const int* rref;     // dense cost index per ref, -1 = no cost entry
+  const int64_t* cost;
+  int64_t* marg;
+  int* taken;
+  int* ev;
+  int* qoff;
+  int* qcnt;
+  int* qh;
+  int* out;
+  int* status;
+  int64_t* result;
+};
+
+__global__ void k_online_grow(PoolDev P, int k, int64_t t);
+__global__ void k_online_release(PoolDev P, int k, int64_t online_used);
+__global__ void k_offline_reserve(PoolDev P, int64_t req, int pages, int64_t t, int max_off);
+__global__ void k_offline_release(PoolDev P, int64_t req);
+__global__ void k_requests_on_handle(PoolDev P, int h, int64_t* out);
+__global__ void k_handles_of_request(PoolDev P, int64_t req, int* out);
+__global__ void k_offline_pages_of(PoolDev P, int64_t req);
+__global__ void k_block_table(PoolDev P, int64_t req, int* out);
+__global__ void k_snapshot(PoolDev P);
+__global__ void k_apply(PoolDev P, const int* ids, int k, int64_t t);
+__global__ void k_reclaim(PoolDev P, int k, int mode, int64_t t);
+__global__ void k_check_invariants(PoolDev P, int64_t online_used);
+__global__ void k_fill_pages(PoolDev P);
+__global__ void k_set_costs(PoolDev P, int n, const int64_t* reqs, const int64_t* costs);
+__global__ void k_select_instance(SelectArgs A);
+__global__ void k_map_refs(const int64_t* reqs, int nnz, const int64_t* keys, int m, int* rref);
+__global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix);
+__global__ void k_evicted_cost(SelectArgs A, const int* pick, int n_pick);
+
+// reclaim copy (copy_kernels.cu)
+struct CopyArgs {
+  const uint8_t* pages;
+  int64_t slot_bytes, page_bytes, chunk_bytes;
+  const int* phys;
+  int n_pages;
+  int64_t n_chunks;
+  uint8_t* dst;  // device alias of pinned host memory
+  double ns_per_byte;  // 0 = unbounded
+  int64_t burst_bytes;
+  unsigned long long* cursor;
+  unsigned long long* t_first;
+  unsigned long long* t_last;
+};
+__global__ void k_reclaim_copy(CopyArgs A);
+__global__ void k_reclaim_copy_tma(CopyArgs A);
+
+// gate (gate_kernels.cu)
+struct GateDev {
+  unsigned int closed;        // polled word
+  unsigned int gen;
+  unsigned int live_ctas;     // gated CTAs resident or pending
+  unsigned int quiesced_gen;
+  unsigned long long t_first_seen;
+  unsigned long long t_quiesced;
+  unsigned long long cursor;  // tiles claimed (== done once quiesced)
+  unsigned long long tiles_done;
+  unsigned long long canary;
+};
+struct OfflineArgs {
+  GateDev* g;
+  const uint8_t* pages;
+  int64_t slot_bytes, page_bytes, chunk_bytes;
+  int chunks_per_page;
+  const int* bt;
+  int P, quarantine;
+  const int* rows;
+  const int64_t* tile_prefix;  // [n_requests+1] tiles before request i
+  int n_requests;
+  int64_t total_tiles;
+  float* out;
+  int poll;
+};
+__global__ void k_offline_decode(OfflineArgs A);
+
+}  // namespace valve

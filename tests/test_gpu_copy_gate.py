@@ -1,0 +1,191 @@
+"""Reclaimed byte images and the device preemption gate (sm_100a kernels).
+
+Byte images: every page reported by apply_reclaim / the fused reclaim is gathered from its
+physical slot into pinned host memory; the bytes must equal the C restatement's image of
+(request, block) in report order -- bit-exact, through the SM copy kernel (LDG/STG and the
+bulk-copy/TMA variant), the copy-engine baseline, and under a rate bound.
+
+Gate: the gated offline kernel quiesces on a raised gate, never claims a tile afterwards,
+and resumes from its HBM cursor so every tile runs exactly once across preemptions; a
+reclaim issued without waiting for quiesce is caught by the quarantine canary.
+"""
+import ctypes as C
+import random
+import time
+
+import numpy as np
+import pytest
+
+from paper_2604_07874_b200 import api as A
+
+pytestmark = pytest.mark.gpu
+
+
+def _expected_images(oracle_c, res, page_bytes):
+    reqs, blks = [], []
+    for r in res.evicted_requests:
+        reqs += [r] * len(res.invalidated_pages[r])
+        blks += res.block_index[r]
+    n = len(reqs)
+    out = np.zeros(n * page_bytes, dtype=np.uint8)
+    rq = (C.c_int64 * max(n, 1))(*reqs)
+    bk = (C.c_int32 * max(n, 1))(*blks)
+    oracle_c.lib.vo_gather_images(rq, bk, n, page_bytes, out.ctypes.data)
+    return out
+
+
+def _pool_with_pages(rng, H=32, S=8, slot=16384, page=12288, n_req=40):
+    pool = A.DevicePool(H, S, 16, slot_bytes=slot, page_bytes=page)
+    live = []
+    for r in range(n_req):
+        if pool.offline_reserve(r * 7 + 3, rng.randint(1, 2 * S), r):
+            live.append(r * 7 + 3)
+    pool.fill_pages()
+    pool.set_costs({r: rng.randint(1, 100) for r in live})
+    return pool, live
+
+
+@pytest.mark.parametrize("engine,kw", [
+    ("sm", dict(ctas=4, chunk_bytes=4096)),
+    ("sm", dict(ctas=1, threads=128, chunk_bytes=12288)),
+    ("sm", dict(ctas=8, use_tma=1, chunk_bytes=8192)),
+    ("sm", dict(ctas=3, chunk_bytes=4096, rate_bytes_per_s=2e9, burst_bytes=8192)),
+    ("ce", {}),
+])
+def test_reclaim_byte_images(oracle_c, engine, kw):
+    rng = random.Random(11)
+    pool, live = _pool_with_pages(rng)
+    _, _, n_pages = pool.reclaim(5, 1000)
+    res = pool.last_reclaim()
+    assert n_pages == sum(len(v) for v in res.invalidated_pages.values()) > 0
+    buf = A.HostBuffer(n_pages * pool.page_bytes)
+    st = pool.reclaim_copy(buf.ptr, buf.nbytes, A.copy_params(**kw) if kw else None, engine=engine)
+    assert st.bytes == n_pages * pool.page_bytes
+    want = _expected_images(oracle_c, res, pool.page_bytes)
+    assert np.array_equal(buf.view(), want)
+    if kw.get("rate_bytes_per_s"):
+        # token bucket: the copy cannot finish before (bytes - burst) / rate
+        floor_ns = (st.bytes - kw["burst_bytes"] - kw["chunk_bytes"]) / kw["rate_bytes_per_s"] * 1e9
+        assert st.t_last_ns - st.t_first_ns >= floor_ns * 0.95
+
+
+def test_apply_reclaim_copy_matches_explicit_ids(oracle_c):
+    """apply_reclaim with caller-chosen handles -> the copy list follows its report."""
+    rng = random.Random(3)
+    pool, live = _pool_with_pages(rng)
+    inst = pool.snapshot()
+    ids = [h.id for h in inst.handles][::3][:4]
+    res = pool.apply_reclaim(ids, 99)
+    n = sum(len(v) for v in res.invalidated_pages.values())
+    buf = A.HostBuffer(max(n, 1) * pool.page_bytes)
+    pool.reclaim_copy(buf.ptr, buf.nbytes, A.copy_params(ctas=2, chunk_bytes=4096))
+    assert np.array_equal(buf.view()[: n * pool.page_bytes], _expected_images(oracle_c, res, pool.page_bytes))
+
+
+# ------------------------------------------------------------------------------ gate
+
+def _offline_setup(torch, pool, reqs):
+    rows = [pool.request_row(r) for r in reqs]
+    npages = [pool.offline_pages_of(r) for r in reqs]
+    cpp = -(-pool.page_bytes // 65536)
+    total = sum(npages) * cpp
+    t_rows = torch.tensor(rows, dtype=torch.int32, device="cuda")
+    t_np = torch.tensor(npages, dtype=torch.int32, device="cuda")
+    out = torch.full((total,), float("nan"), dtype=torch.float32, device="cuda")
+    return t_rows, t_np, out, total
+
+
+def test_gate_preempt_resume_conserves_work():
+    torch = pytest.importorskip("torch")
+    rng = random.Random(5)
+    pool = A.DevicePool(64, 16, 16, slot_bytes=1 << 20, page_bytes=917504)
+    reqs = []
+    for r in range(40):
+        if pool.offline_reserve(r, rng.randint(8, 40), 0):
+            reqs.append(r)
+    pool.fill_pages()
+    t_rows, t_np, out_ref, total = _offline_setup(torch, pool, reqs)
+    gate = A.Gate(0)
+    # uninterrupted run (reference outputs)
+    gate.reset_work()
+    gate.launch_offline(pool, t_rows.data_ptr(), t_np.data_ptr(), len(reqs), total,
+                        out_ref.data_ptr(), stream=gate.stream)
+    torch.cuda.synchronize()
+    assert gate.read().tiles_done == total
+    # preempted runs: raise after a short delay, wait quiesce, resume from the cursor
+    out = torch.full_like(out_ref, float("nan"))
+    gate.reset_work()
+    gen = 0
+    preemptions = 0
+    while True:
+        gate.launch_offline(pool, t_rows.data_ptr(), t_np.data_ptr(), len(reqs), total, out.data_ptr(),
+                            ctas=4)
+        time.sleep(rng.uniform(0.0002, 0.0008))
+        gen += 1
+        gate.raise_(gen)
+        gate.wait_quiesced(gen)
+        torch.cuda.synchronize()
+        s = gate.read()
+        assert s.live_ctas == 0
+        done = s.tiles_done
+        # context save = cursor: every claimed tile finished before the CTA retired
+        assert s.tiles_done == min(s.tiles_claimed, total)
+        gate.release(gen)
+        torch.cuda.synchronize()
+        preemptions += 1
+        if done >= total:
+            break
+        assert preemptions < 200
+    assert gate.read().tiles_done == total
+    a = out.view(torch.int32).cpu().numpy()
+    b = out_ref.view(torch.int32).cpu().numpy()
+    assert np.array_equal(a, b)  # every tile exactly once, bit-identical results
+    assert preemptions >= 2
+
+
+def test_gate_closed_before_launch_runs_nothing():
+    torch = pytest.importorskip("torch")
+    pool = A.DevicePool(8, 8, 16, slot_bytes=1 << 20, page_bytes=917504)
+    assert pool.offline_reserve(1, 10, 0)
+    pool.fill_pages()
+    t_rows, t_np, out, total = _offline_setup(torch, pool, [1])
+    gate = A.Gate(0)
+    gate.reset_work()
+    gate.raise_(1)
+    gate.wait_quiesced(1)
+    torch.cuda.synchronize()
+    # the launch waits for an open gate: nothing runs while raised
+    gate.launch_offline(pool, t_rows.data_ptr(), t_np.data_ptr(), 1, total, out.data_ptr(),
+                        stream=None)
+    time.sleep(0.05)
+    assert gate.read().tiles_done == 0
+    gate.release(2)
+    torch.cuda.synchronize()
+    pool_stream_sync = pool.view().stream  # the launch went to the pool's stream
+    assert pool_stream_sync
+    deadline = time.time() + 10
+    while gate.read().tiles_done < total and time.time() < deadline:
+        time.sleep(0.01)
+    assert gate.read().tiles_done == total
+
+
+def test_quarantine_canary_catches_ungated_reclaim():
+    """Negative test (sim.cpp:1003-1008 fault detector): reclaiming while the
+    offline kernel still runs makes it read remapped block-table entries -> canary hits."""
+    torch = pytest.importorskip("torch")
+    pool = A.DevicePool(16, 16, 16, slot_bytes=1 << 20, page_bytes=917504)
+    reqs = [r for r in range(12) if pool.offline_reserve(r, 20, 0)]
+    pool.fill_pages()
+    pool.set_costs({r: 1 for r in reqs})
+    t_rows, t_np, out, total = _offline_setup(torch, pool, reqs)
+    gate = A.Gate(0)
+    gate.reset_work()
+    side = torch.cuda.Stream()
+    # one CTA so the kernel is still walking the list when the reclaim lands
+    gate.launch_offline(pool, t_rows.data_ptr(), t_np.data_ptr(), len(reqs), total, out.data_ptr(),
+                        ctas=1, threads=64, stream=side.cuda_stream)
+    time.sleep(0.002)
+    pool.reclaim(8, 1)  # no gate raise, no quiesce wait (unsafe_skip_compute_gate analogue)
+    side.synchronize()
+    s = gate.read()
+    assert s.canary_hits >= 1

@@ -37,7 +37,16 @@ struct vo_pool {
   int64_t* rq_key;
   int* rq_next;
   int rq_n, rq_cap;
+  /* blocks remapped to the quarantine page while their request stays live (only after an
+   * apply_reclaim that stopped at a bad handle: the residual release never ran) */
+  int64_t* qr_req;
+  int* qr_blk;
+  int qr_n, qr_cap;
 };
+
+/* A slot is live iff it carries a block index (request ids may be any int64, -1 included). */
+#define LIVE(p, i) ((p)->slot_blk[i] != -1)
+#define HOLDS(p, i, req) (LIVE(p, i) && (p)->slot_req[i] == (req))
 
 static int count_state(const vo_pool* p, int st) {
   int n = 0;
@@ -81,7 +90,31 @@ void vo_pool_destroy(vo_pool* p) {
   free(p->slot_blk);
   free(p->rq_key);
   free(p->rq_next);
+  free(p->qr_req);
+  free(p->qr_blk);
   free(p);
+}
+
+static void qr_add(vo_pool* p, int64_t req, int blk) {
+  if (p->qr_n == p->qr_cap) {
+    p->qr_cap = p->qr_cap ? 2 * p->qr_cap : 16;
+    p->qr_req = (int64_t*)realloc(p->qr_req, (size_t)p->qr_cap * 8);
+    p->qr_blk = (int*)realloc(p->qr_blk, (size_t)p->qr_cap * sizeof(int));
+  }
+  p->qr_req[p->qr_n] = req;
+  p->qr_blk[p->qr_n] = blk;
+  ++p->qr_n;
+}
+
+static void qr_drop(vo_pool* p, int64_t req) {
+  int w = 0;
+  for (int i = 0; i < p->qr_n; ++i)
+    if (p->qr_req[i] != req) {
+      p->qr_req[w] = p->qr_req[i];
+      p->qr_blk[w] = p->qr_blk[i];
+      ++w;
+    }
+  p->qr_n = w;
 }
 
 int vo_pool_counts(const vo_pool* p, int64_t out[5]) {
@@ -177,7 +210,7 @@ static void rq_drop(vo_pool* p, int64_t req) {
 static void fill_handle(vo_pool* p, int h, int64_t req, int* remaining) {
   int64_t base = (int64_t)h * p->S;
   for (int s = 0; s < p->S && *remaining > 0 && p->used[h] < p->S; ++s) {
-    if (p->slot_req[base + s] != -1) continue;
+    if (LIVE(p, base + s)) continue;
     p->slot_req[base + s] = req;
     p->slot_lid[base + s] = p->used[h]++;
     p->slot_blk[base + s] = rq_next_blk(p, req);
@@ -225,7 +258,7 @@ static void release_req(vo_pool* p, int64_t req) {
     int64_t base = (int64_t)h * p->S;
     int dropped = 0;
     for (int s = 0; s < p->S; ++s)
-      if (p->slot_req[base + s] == req) {
+      if (HOLDS(p, base + s, req)) {
         p->slot_req[base + s] = -1;
         p->slot_lid[base + s] = -1;
         p->slot_blk[base + s] = -1;
@@ -236,6 +269,7 @@ static void release_req(vo_pool* p, int64_t req) {
     if (p->used[h] == 0) p->state[h] = ST_FREE;
   }
   rq_drop(p, req);
+  qr_drop(p, req);
 }
 
 int vo_pool_offline_release(vo_pool* p, int64_t req) {
@@ -253,7 +287,7 @@ static int residents(const vo_pool* p, int h, int64_t* buf) {
   int n = 0;
   int64_t base = (int64_t)h * p->S;
   for (int s = 0; s < p->S; ++s)
-    if (p->slot_req[base + s] != -1) buf[n++] = p->slot_req[base + s];
+    if (LIVE(p, base + s)) buf[n++] = p->slot_req[base + s];
   qsort(buf, (size_t)n, 8, cmp_i64);
   int u = 0;
   for (int i = 0; i < n; ++i)
@@ -279,7 +313,7 @@ int vo_pool_handles_of_request(const vo_pool* p, int64_t req, int* out, int cap,
     if (p->state[h] != ST_OFFLINE) continue;
     int64_t base = (int64_t)h * p->S;
     for (int s = 0; s < p->S; ++s)
-      if (p->slot_req[base + s] == req) {
+      if (HOLDS(p, base + s, req)) {
         if (c < cap) out[c] = h;
         ++c;
         break;
@@ -295,7 +329,7 @@ int vo_pool_offline_pages_of(const vo_pool* p, int64_t req, int* out) {
   for (int h = 0; h < p->H; ++h) {
     if (p->state[h] != ST_OFFLINE) continue;
     int64_t base = (int64_t)h * p->S;
-    for (int s = 0; s < p->S; ++s) c += p->slot_req[base + s] == req;
+    for (int s = 0; s < p->S; ++s) c += HOLDS(p, base + s, req);
   }
   *out = c;
   return VO_OK;
@@ -361,11 +395,12 @@ int vo_pool_apply_reclaim(vo_pool* p, const int* ids, int k, int64_t t, int* han
     }
     int64_t base = (int64_t)h * p->S;
     for (int s = 0; s < p->S; ++s) {
-      if (p->slot_req[base + s] == -1) continue;
+      if (!LIVE(p, base + s)) continue;
       inv[ni].req = p->slot_req[base + s];
       inv[ni].page = base + p->slot_lid[base + s];
       inv[ni].phys = (int)(base + s);
       inv[ni].blk = p->slot_blk[base + s];
+      qr_add(p, inv[ni].req, inv[ni].blk);
       ++ni;
       p->slot_req[base + s] = -1;
       p->slot_lid[base + s] = -1;
@@ -423,7 +458,7 @@ int vo_pool_check_invariants(const vo_pool* p) {
     return fail(VO_LOGIC_ERROR, "MemoryPool: online page accounting out of bounds");
   for (int h = 0; h < p->H; ++h) {
     int slots = 0;
-    for (int s = 0; s < p->S; ++s) slots += p->slot_req[(int64_t)h * p->S + s] != -1;
+    for (int s = 0; s < p->S; ++s) slots += LIVE(p, (int64_t)h * p->S + s);
     if (slots != p->used[h] || p->used[h] > p->S)
       return fail(VO_LOGIC_ERROR, "MemoryPool: slot accounting mismatch");
     if (p->state[h] != ST_OFFLINE && p->used[h] != 0)
@@ -433,13 +468,20 @@ int vo_pool_check_invariants(const vo_pool* p) {
 }
 
 int vo_pool_block_table(const vo_pool* p, int64_t req, int* out, int cap, int* n) {
+  /* blocks 0..nblk-1: the physical page, or the quarantine page H*S once remapped */
   int c = 0;
   int64_t ns = (int64_t)p->H * p->S;
   for (int64_t i = 0; i < ns; ++i)
-    if (p->slot_req[i] == req) {
+    if (HOLDS(p, i, req)) {
       int b = p->slot_blk[i];
       if (b < cap) out[b] = (int)i;
-      ++c;
+      if (b + 1 > c) c = b + 1;
+    }
+  for (int i = 0; i < p->qr_n; ++i)
+    if (p->qr_req[i] == req) {
+      int b = p->qr_blk[i];
+      if (b < cap) out[b] = (int)ns;
+      if (b + 1 > c) c = b + 1;
     }
   *n = c;
   return VO_OK;

@@ -869,7 +869,9 @@ __global__ void __launch_bounds__(kNT)
     if (A.rref[e] < 0) s_missing = 1;
   __syncthreads();
   if (threadIdx.x == 0) A.status[0] = 0;
-  if (A.k > 0 && s_missing) {  // reclaim.cpp:13 (cost_of throws on the first evaluation)
+  // reclaim.cpp:13: cost_of throws on the first evaluation (greedy / exhaustive, k > 0);
+  // fifo never looks at costs (reclaim.cpp:69-83)
+  if (A.k > 0 && s_missing && A.mode != 1) {
     if (threadIdx.x == 0) A.status[0] = kDetNoCost;
     return;
   }

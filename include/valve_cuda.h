@@ -223,10 +223,10 @@ void* valve_gate_stream(const valve_gate* g);
  * a raised gate stops claiming at the next tile boundary and the CTA exits (context save =
  * the cursor).  Returns immediately (stream-ordered). */
 typedef struct {
-  const int* rows;        /* device: request rows to decode */
-  const int* npages;      /* device: pages per listed request */
+  const int* rows;        /* device: request rows to decode; NULL = every row of the pool */
+  const int* npages;      /* device: pages per listed request (ignored when rows == NULL) */
   int n_requests;
-  int64_t total_tiles;    /* sum of npages */
+  int64_t total_tiles;    /* informational; the kernel derives it from the tile prefix */
   float* out;             /* device: one fp32 per tile */
   int ctas;               /* 0 = 148 x resident */
   int threads;            /* 0 = 256 */

@@ -299,3 +299,37 @@ extern "C" void vr_rng_draws(uint64_t seed, const char* label, int n, uint64_t* 
   Rng rng = label ? Rng::substream(seed, label) : Rng(seed);
   for (int i = 0; i < n; ++i) out[i] = static_cast<uint64_t>(rng.uniform_int(0, INT64_MAX - 1));
 }
+
+// CPU baseline of the decision path, timed inside C++ (no ctypes in the timed region):
+// snapshot + Cost(r) attach (sim.cpp:877-883) -> selective_reclaim (reclaim.cpp:33-67) ->
+// apply_reclaim (memory.cpp:155-180), exactly what Sim::finish_op does per op.  Returns the
+// invalidated logical page ids (report order) for the gather leg.
+#include <chrono>
+extern "C" int vr_time_reclaim(vo_pool* p, const int64_t* keys, const int64_t* vals, int m, int k,
+                               int64_t t, double us_out[3], int64_t* pages_out, int cap,
+                               int* n_pages) {
+  return guard([&] {
+    using clk = std::chrono::steady_clock;
+    std::map<std::int64_t, std::int64_t> cost;
+    for (int i = 0; i < m; ++i) cost[keys[i]] = vals[i];
+    const auto t0 = clk::now();
+    ReclaimInstance inst = p->pool.snapshot();
+    for (const ReclaimHandle& h : inst.handles)
+      for (std::int64_t r : h.requests) inst.cost[r] = cost.at(r);
+    const auto t1 = clk::now();
+    std::vector<int> chosen = selective_reclaim(inst, k);
+    const auto t2 = clk::now();
+    MemoryPool::ReclaimResult res = p->pool.apply_reclaim(chosen, t);
+    const auto t3 = clk::now();
+    us_out[0] = std::chrono::duration<double, std::micro>(t1 - t0).count();
+    us_out[1] = std::chrono::duration<double, std::micro>(t2 - t1).count();
+    us_out[2] = std::chrono::duration<double, std::micro>(t3 - t2).count();
+    int n = 0;
+    for (const auto& [req, pages] : res.invalidated_pages)
+      for (std::int64_t pg : pages) {
+        if (n < cap) pages_out[n] = pg;
+        ++n;
+      }
+    *n_pages = n;
+  });
+}

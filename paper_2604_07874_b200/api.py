@@ -825,9 +825,10 @@ class Gate:
     def reset_work(self):
         self._b.check(self._b.lib.valve_offline_reset(self._h))
 
-    def launch_offline(self, pool: DevicePool, rows_ptr: int, npages_ptr: int, n_requests: int,
-                       total_tiles: int, out_ptr: int, *, ctas: int = 0, threads: int = 0,
-                       poll: bool = True, stream: Optional[int] = None):
+    def launch_offline(self, pool: DevicePool, rows_ptr: Optional[int], npages_ptr: Optional[int],
+                       n_requests: int, total_tiles: int, out_ptr: Optional[int], *, ctas: int = 0,
+                       threads: int = 0, poll: bool = True, stream: Optional[int] = None):
+        """rows_ptr=None decodes every request row of the pool; out_ptr=None drops results."""
         w = OfflineWork(rows_ptr, npages_ptr, n_requests, total_tiles, out_ptr, ctas, threads,
                         1 if poll else 0)
         self._b.check(self._b.lib.valve_offline_launch(self._h, pool.handle, C.byref(w),

@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(256) k_offline_decode(OfflineArgs A) {
       if (!stop) tile = (long long)atomicAdd(&A.g->cursor, 1ull);
     }
     tile = __shfl_sync(kFull, tile, 0);
-    if (tile < 0 || tile >= A.total_tiles) break;
+    if (tile < 0 || tile >= A.tile_prefix[A.n_requests]) break;
     // locate (request, page, chunk): binary search over the tile prefix
     int lo = 0, hi = A.n_requests - 1;
     while (lo < hi) {
@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(256) k_offline_decode(OfflineArgs A) {
     const int64_t local = tile - A.tile_prefix[lo];
     const int page = (int)(local / A.chunks_per_page);
     const int64_t off = (local % A.chunks_per_page) * A.chunk_bytes;
-    const int phys = A.bt[(int64_t)A.rows[lo] * A.P + page];
+    const int row = A.rows ? A.rows[lo] : lo;  // rows == nullptr: every request row
+    const int phys = A.bt[(int64_t)row * A.P + page];
     float acc = 0.f;
     if (phys == A.quarantine || phys < 0) {
       if (lane == 0) atomicAdd(&A.g->canary, 1ull);
@@ -104,7 +105,8 @@ __global__ void __launch_bounds__(256) k_offline_decode(OfflineArgs A) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
     if (lane == 0) {
-      A.out[tile] = acc;
+      if (A.out) A.out[tile] = acc;
+      else if (acc == 1.2345e-30f) atomicAdd(&A.g->canary, 0ull);  // keeps the loads live
       atomicAdd(&A.g->tiles_done, 1ull);
     }
   }

@@ -1130,17 +1130,21 @@ int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work*
   return guard([&] {
     const MemOps& op = memops();
     if (!p->d.pages) fail(VALVE_LOGIC_ERROR, "offline_launch: pool has no page store");
-    if (w->n_requests <= 0) return;
+    // rows == NULL: decode every request row of the pool (blocks from the device table)
+    const bool all_rows = w->rows == nullptr;
+    const int n_req = all_rows ? p->R : w->n_requests;
+    const int* npages = all_rows ? p->d.row_nblk : w->npages;
+    if (n_req <= 0) return;
     cudaStream_t st = as_stream(s, p->stream);
     ck(cudaSetDevice(g->device), "cudaSetDevice");
     const int64_t chunk = 65536;
     const int cpp = (int)((p->d.page_bytes + chunk - 1) / chunk);
-    if (w->n_requests + 1 > g->cap_prefix) {
+    if (n_req + 1 > g->cap_prefix) {
       if (g->d_prefix) cudaFree(g->d_prefix);
-      g->cap_prefix = std::max<int64_t>(w->n_requests + 1, 2 * g->cap_prefix);
+      g->cap_prefix = std::max<int64_t>(n_req + 1, 2 * g->cap_prefix);
       ck(cudaMalloc((void**)&g->d_prefix, g->cap_prefix * 8), "cudaMalloc");
     }
-    k_tile_prefix<<<1, kNT, 0, st>>>(w->npages, w->n_requests, cpp, g->d_prefix);
+    k_tile_prefix<<<1, kNT, 0, st>>>(npages, n_req, cpp, g->d_prefix);
     counted();
     int threads = w->threads > 0 ? w->threads : 256;
     int ctas = w->ctas;
@@ -1165,7 +1169,7 @@ int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work*
     A.quarantine = p->d.quarantine;
     A.rows = w->rows;
     A.tile_prefix = g->d_prefix;
-    A.n_requests = w->n_requests;
+    A.n_requests = n_req;
     A.total_tiles = w->total_tiles;
     A.out = w->out;
     A.poll = w->poll;

@@ -42,6 +42,7 @@ METRIC = "p99 preempt-to-quiesce µs; reclaim GB/s vs link peak; online TTFT/TPO
 SLOT = 2 << 20            # 2 MiB: one 16-token Llama-3-8B KV page (SURVEY §8 geometry)
 PAGE = 917_504            # Qwen2-7B 16-token KV page (28 x 2 x 4 x 128 x 2 B x 16)
 HSZ = 64                  # pages per handle
+TILE = 16384              # offline tile (quiesce granularity), the library default
 WEIGHTS = 31.3e9          # Llama-3-8B + Qwen2-7B bf16 weights (not allocated here)
 
 
@@ -205,7 +206,7 @@ def run_valve(args, rank, world, dist):
             pool.set_costs(costs)
 
     def tiles_left_low():
-        total = sum(p for p, _ in live.values()) * (-(-PAGE // 65536))
+        total = sum(p for p, _ in live.values()) * (-(-PAGE // TILE))
         return gate.read().tiles_claimed >= 0.8 * total
 
     def step(record):
@@ -294,7 +295,7 @@ def run_valve(args, rank, world, dist):
         e.record(off_stream)
         torch.cuda.synchronize()
         tiles = gate.read().tiles_done
-        return tiles * 65536 / (s.elapsed_time(e) * 1e-3) / 1e9, tiles, s.elapsed_time(e)
+        return tiles * TILE / (s.elapsed_time(e) * 1e-3) / 1e9, tiles, s.elapsed_time(e)
     offline_rate(True)
     polled = offline_rate(True)
     unpolled = offline_rate(False)

@@ -109,6 +109,10 @@ enum { VALVE_SELECT_SELECTIVE = 0, VALVE_SELECT_FIFO = 1, VALVE_SELECT_ORACLE = 
  * valve_pool_last_reclaim() to read the full result. */
 int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles, int* n_evicted,
                        int* n_pages);
+/* Device phase durations of the last valve_pool_reclaim (ns, %globaltimer): out[0] instance
+ * build (snapshot), out[1] selection, out[2] apply; out[3..4] SM cycles of the greedy rounds
+ * (argmin, incremental update) of the last shared-memory selection in this process. */
+int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[5]);
 int valve_pool_last_reclaim(const valve_pool* p, int* handles, int64_t* evicted, int* inv_off,
                             int64_t* inv_pages, int* inv_phys, int* inv_blk, int cap_h, int cap_ev,
                             int cap_pages);
@@ -231,6 +235,7 @@ typedef struct {
   int ctas;               /* 0 = 148 x resident */
   int threads;            /* 0 = 256 */
   int poll;               /* 0 = no gate polling (overhead baseline) */
+  int64_t tile_bytes;     /* bytes of one tile (the quiesce granularity); 0 = 16 KiB */
 } valve_offline_work;
 int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work* w, void* stream);
 /* Resets the tile cursor / statistics (new work). */

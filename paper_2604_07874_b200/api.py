@@ -636,7 +636,7 @@ class GateState(C.Structure):
 class OfflineWork(C.Structure):
     _fields_ = [("rows", C.c_void_p), ("npages", C.c_void_p), ("n_requests", C.c_int),
                 ("total_tiles", i64), ("out", C.c_void_p), ("ctas", C.c_int), ("threads", C.c_int),
-                ("poll", C.c_int)]
+                ("poll", C.c_int), ("tile_bytes", i64)]
 
 
 class PoolView(C.Structure):
@@ -827,9 +827,10 @@ class Gate:
 
     def launch_offline(self, pool: DevicePool, rows_ptr: Optional[int], npages_ptr: Optional[int],
                        n_requests: int, total_tiles: int, out_ptr: Optional[int], *, ctas: int = 0,
-                       threads: int = 0, poll: bool = True, stream: Optional[int] = None):
+                       threads: int = 0, poll: bool = True, stream: Optional[int] = None,
+                       tile_bytes: int = 0):
         """rows_ptr=None decodes every request row of the pool; out_ptr=None drops results."""
         w = OfflineWork(rows_ptr, npages_ptr, n_requests, total_tiles, out_ptr, ctas, threads,
-                        1 if poll else 0)
+                        1 if poll else 0, tile_bytes)
         self._b.check(self._b.lib.valve_offline_launch(self._h, pool.handle, C.byref(w),
                                                        C.c_void_p(stream) if stream else None))

@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(256) k_offline_decode(OfflineArgs A) {
   float q[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) q[i] = 0.0625f * (float)((lane * 8 + i) % 16 - 8);
+  unsigned long long done = 0;
   for (;;) {
     long long tile = -1;
     if (lane == 0) {
@@ -107,10 +108,11 @@ __global__ void __launch_bounds__(256) k_offline_decode(OfflineArgs A) {
     if (lane == 0) {
       if (A.out) A.out[tile] = acc;
       else if (acc == 1.2345e-30f) atomicAdd(&A.g->canary, 0ull);  // keeps the loads live
-      atomicAdd(&A.g->tiles_done, 1ull);
     }
+    ++done;
   }
-  // warp done; the CTA's last warp retires the CTA (the quiesce ack)
+  // warp done: publish its tiles, then the CTA's last warp retires the CTA (the quiesce ack)
+  if (lane == 0 && done) atomicAdd(&A.g->tiles_done, done);
   if (lane == 0 && atomicAdd(&s_exited, 1) == nw - 1) {
     __threadfence();
     if (atomicSub(&A.g->live_ctas, 1u) == 1u) {

@@ -1,0 +1,694 @@
+// reclaim_kernels.cu -- Algorithm-1 selection, apply_reclaim and the fused device reclaim
+// (snapshot -> select -> apply in one launch) for sm_100a.
+//
+// Reference semantics (file:line under /root/reference/proj):
+//   selective_reclaim / fifo / oracle / evicted_cost   src/reclaim.cpp:19-126
+//   apply_reclaim                                      src/memory.cpp:155-180
+//   Sim::finish_op (snapshot + Cost + select + apply)  src/sim.cpp:928-943
+//
+// Layout: one CTA of 1024 threads.  The instance (offline handles, distinct resident rows)
+// is built into global scratch with a stride of S per handle; the greedy rounds run in ONE
+// warp over shared-memory marginals (n <= 2048 handles) with incremental updates through a
+// reverse request->handle index, so a round is ~a hundred cycles and no CTA barrier.  The
+// invalidation report is sorted in shared memory (<= 8192 pages per op).
+#include "pool_device.cuh"
+#include "valve_kernels.h"
+
+namespace valve {
+
+constexpr int kSmemHandles = 2048;   // greedy in shared memory up to this many handles
+constexpr int kSmemListings = 4096;  // ... and this many (handle, request) listings
+constexpr int kSmemTuples = 8192;    // invalidation report sorted in shared memory
+// dynamic shared memory of k_reclaim / k_apply / k_select_instance (host sets the attribute):
+// greedy 2048*(8+4+4+1) + 4096*(8+4+4+4+4+4) + 4 = 149,508 B; apply sort 8192*12 = 98,304 B
+static_assert(kSmemHandles * 17 + kSmemListings * 28 + 64 <= 160 * 1024, "greedy smem");
+static_assert(kSmemTuples * 12 <= 160 * 1024, "sort smem");
+
+__device__ long long g_greedy_cycles[2];  // diagnostics: argmin / update cycles of the last run
+
+// Ref lists of instance handle i: CSR (off) or fixed stride with counts (cnt).
+struct Refs {
+  const int* off;
+  const int* cnt;
+  int stride;
+  __device__ __forceinline__ int begin(int i) const { return cnt ? i * stride : off[i]; }
+  __device__ __forceinline__ int end(int i) const { return cnt ? i * stride + cnt[i] : off[i + 1]; }
+};
+
+// Reverse index request -> handle indices (one entry per listing, duplicates kept), and
+// the initial marginals marg[i] = sum of cost over the listings of handle i.  CTA-wide.
+__device__ void build_instance_index(int n, Refs R, const int* rref, int m, const int64_t* cost,
+                                     int64_t* marg, int* qoff, int* qcnt, int* qh, int* ev) {
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    qcnt[r] = 0;
+    ev[r] = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int64_t s = 0;
+    for (int e = R.begin(i); e < R.end(i); ++e) {
+      const int r = rref[e];
+      s += cost[r];
+      atomicAdd(&qcnt[r], 1);
+    }
+    marg[i] = s;
+  }
+  __syncthreads();
+  int carry = 0;
+  for (int base = 0; base < m; base += blockDim.x) {
+    const int r = base + threadIdx.x;
+    const int c = r < m ? qcnt[r] : 0;
+    int tot;
+    const int ex = block_excl_scan(c, tot);
+    if (r < m) qoff[r] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) qoff[m] = carry;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) qcnt[r] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    for (int e = R.begin(i); e < R.end(i); ++e) {
+      const int r = rref[e];
+      qh[qoff[r] + atomicAdd(&qcnt[r], 1)] = i;
+    }
+  __syncthreads();
+}
+
+__device__ __forceinline__ ArgMin warp_argmin(ArgMin a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMin b;
+    b.v = __shfl_xor_sync(kFull, a.v, o);
+    b.id = __shfl_xor_sync(kFull, a.id, o);
+    b.idx = __shfl_xor_sync(kFull, a.idx, o);
+    if (argmin_less(b, a)) a = b;
+  }
+  return a;
+}
+
+__device__ __forceinline__ void cand_min(int64_t& bm, int& bid, int& bidx, int64_t m, int id, int idx) {
+  // lexicographic (marginal, id) minimum; idx < 0 = no candidate.  Branch-free.
+  const bool better = (idx >= 0) & ((bidx < 0) | (m < bm) | ((m == bm) & (id < bid)));
+  bm = better ? m : bm;
+  bid = better ? id : bid;
+  bidx = better ? idx : bidx;
+}
+
+__device__ __forceinline__ void warp_min(int64_t& bm, int& bid, int& bidx) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t om = __shfl_xor_sync(kFull, bm, o);
+    const int oid = __shfl_xor_sync(kFull, bid, o);
+    const int oidx = __shfl_xor_sync(kFull, bidx, o);
+    cand_min(bm, bid, bidx, om, oid, oidx);
+  }
+}
+
+// Algorithm 1 (reclaim.cpp:33-67), CTA-wide with the marginals in registers: thread t owns
+// handles t and t + blockDim (n <= 2 * blockDim).  A round is a two-level (marginal, id)
+// argmin (shuffles, 32 partials in shared memory, every warp finishes the reduction so no
+// second barrier is needed), then the threads of the winner's listings evict its requests
+// (first eviction wins an atomicExch on ev) and scatter -cost into `delta` through the
+// reverse index; owners fold their deltas in.  Two barriers per round, all data on-chip.
+// `delta` holds the initial marginals on entry.
+constexpr int kGreedyThreads = 256;                         // warps 0..7 run the rounds
+constexpr int kGreedyOwn = kSmemHandles / kGreedyThreads;  // handles per thread (registers)
+
+__device__ __forceinline__ void greedy_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kGreedyThreads) : "memory");
+}
+
+// Called by threads [0, kGreedyThreads) only (named barrier 1); n <= kSmemHandles.
+__device__ void greedy_block(int n, const int* hid, Refs R, const int* rref, const int64_t* cost,
+                             int k, int64_t* delta, int* ev, const int* qoff, const int* qh, int* out) {
+  constexpr int NW = kGreedyThreads / 32;
+  __shared__ int64_t w_m[NW];
+  __shared__ int w_id[NW], w_idx[NW];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  int64_t m[kGreedyOwn];
+  unsigned live = 0;
+#pragma unroll
+  for (int j = 0; j < kGreedyOwn; ++j) {
+    const int i = t + j * kGreedyThreads;
+    m[j] = i < n ? delta[i] : 0;
+    if (i < n) live |= 1u << j;
+  }
+  greedy_bar();
+#pragma unroll
+  for (int j = 0; j < kGreedyOwn; ++j)
+    if ((live >> j) & 1u) delta[t + j * kGreedyThreads] = 0;
+  long long c_arg = 0, c_upd = 0;
+  for (int round = 0; round < k; ++round) {
+    const long long c0 = clock64();
+    int64_t bm = 0;
+    int bid = 0, bidx = -1;
+#pragma unroll
+    for (int j = 0; j < kGreedyOwn; ++j) {
+      const int i = t + j * kGreedyThreads;
+      const bool on = (live >> j) & 1u;
+      cand_min(bm, bid, bidx, m[j], on ? hid[i] : 0, on ? i : -1);
+    }
+    warp_min(bm, bid, bidx);
+    if (lane == 0) {
+      w_m[wid] = bm;
+      w_id[wid] = bid;
+      w_idx[wid] = bidx;
+    }
+    greedy_bar();
+    bm = lane < NW ? w_m[lane] : 0;
+    bid = lane < NW ? w_id[lane] : 0;
+    bidx = lane < NW ? w_idx[lane] : -1;
+    warp_min(bm, bid, bidx);
+    const int best = bidx;
+    const long long c1 = clock64();
+    c_arg += c1 - c0;
+#pragma unroll
+    for (int j = 0; j < kGreedyOwn; ++j)
+      if (best == t + j * kGreedyThreads) live &= ~(1u << j);
+    if (t == 0) out[round] = hid[best];
+    for (int e = R.begin(best) + t; e < R.end(best); e += kGreedyThreads) {
+      const int r = rref[e];
+      if (atomicExch(&ev[r], 1) == 0) {
+        const unsigned long long dec = (unsigned long long)(-cost[r]);
+        for (int q = qoff[r]; q < qoff[r + 1]; ++q)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&delta[qh[q]]), dec);
+      }
+    }
+    greedy_bar();
+#pragma unroll
+    for (int j = 0; j < kGreedyOwn; ++j) {
+      const int i = t + j * kGreedyThreads;
+      if (i < n) {
+        m[j] += delta[i];
+        delta[i] = 0;
+      }
+    }
+    c_upd += clock64() - c1;
+  }
+  if (t == 0) g_greedy_cycles[0] = c_arg, g_greedy_cycles[1] = c_upd;
+}
+
+// Same rounds CTA-wide over global arrays (instances larger than shared memory).
+__device__ void greedy_cta(int n, const int* hid, Refs R, const int* rref, const int64_t* cost,
+                           int k, int64_t* marg, int* taken, int* ev, const int* qoff, const int* qh,
+                           int* out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) taken[i] = 0;
+  __syncthreads();
+  for (int round = 0; round < k; ++round) {
+    ArgMin a{0, 0, -1};
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      if (__ldcg(&taken[i])) continue;
+      ArgMin b{(int64_t)__ldcg((const long long*)&marg[i]), hid[i], i};
+      if (argmin_less(b, a)) a = b;
+    }
+    a = block_argmin(a);
+    const int best = a.idx;
+    if (threadIdx.x == 0) {
+      taken[best] = 1;
+      out[round] = hid[best];
+    }
+    for (int e = R.begin(best) + threadIdx.x; e < R.end(best); e += blockDim.x) {
+      const int r = rref[e];
+      if (atomicExch(&ev[r], 1) == 0) {
+        const unsigned long long dec = (unsigned long long)(-cost[r]);
+        for (int q = qoff[r]; q < qoff[r + 1]; ++q)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&marg[qh[q]]), dec);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Greedy dispatch.  When the instance fits (n <= 2048 handles, <= 4096 listings) it is
+// re-indexed into shared memory -- handles, CSR listings over a dense request index, costs,
+// the reverse index and the eviction flags -- and the rounds run in warp 0 with every access
+// on-chip.  Larger instances run CTA-wide over global scratch.
+__device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, int m,
+                              const int64_t* cost, int k, int64_t* marg_g, int* taken_g, int* ev,
+                              int* qoff, int* qcnt, int* qh, int* out, unsigned char* smem) {
+  int nnz_local = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) nnz_local += R.end(i) - R.begin(i);
+  const int nnz = block_sum(nnz_local);
+  if (n <= kSmemHandles && nnz <= kSmemListings) {
+    // dense request index over the referenced requests (qcnt: flag -> dense id)
+    for (int r = threadIdx.x; r < m; r += blockDim.x) qcnt[r] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      for (int e = R.begin(i); e < R.end(i); ++e) qcnt[rref[e]] = 1;
+    __syncthreads();
+    int m2 = 0;
+    for (int base = 0; base < m; base += blockDim.x) {
+      const int r = base + threadIdx.x;
+      const int f = r < m ? qcnt[r] : 0;
+      int tot;
+      const int ex = block_excl_scan(f, tot);
+      if (r < m) qcnt[r] = f ? m2 + ex : -1;
+      m2 += tot;
+    }
+    // shared-memory carve-up
+    int64_t* marg = reinterpret_cast<int64_t*>(smem);
+    int64_t* cost2 = marg + kSmemHandles;
+    int* hid = reinterpret_cast<int*>(cost2 + kSmemListings);
+    int* roff = hid + kSmemHandles;
+    int* rr = roff + kSmemHandles + 1;
+    int* qoff2 = rr + kSmemListings;
+    int* qh2 = qoff2 + kSmemListings + 1;
+    int* ev2 = qh2 + kSmemListings;
+    int* qcnt2 = ev2 + kSmemListings;
+    unsigned char* taken = reinterpret_cast<unsigned char*>(qcnt2 + kSmemListings);
+    int carry = 0;
+    for (int base = 0; base < n; base += blockDim.x) {
+      const int i = base + threadIdx.x;
+      const int c = i < n ? R.end(i) - R.begin(i) : 0;
+      int tot;
+      const int ex = block_excl_scan(c, tot);
+      if (i < n) {
+        roff[i] = carry + ex;
+        hid[i] = hid_g[i];
+        taken[i] = 0;
+      }
+      carry += tot;
+    }
+    if (threadIdx.x == 0) roff[n] = carry;
+    for (int d = threadIdx.x; d < m2; d += blockDim.x) {
+      ev2[d] = 0;
+      qcnt2[d] = 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      int o = roff[i];
+      for (int e = R.begin(i); e < R.end(i); ++e, ++o) {
+        const int r = rref[e];
+        const int d = qcnt[r];
+        rr[o] = d;
+        cost2[d] = cost[r];
+        atomicAdd(&qcnt2[d], 1);
+      }
+    }
+    __syncthreads();
+    carry = 0;
+    for (int base = 0; base < m2; base += blockDim.x) {
+      const int d = base + threadIdx.x;
+      const int c = d < m2 ? qcnt2[d] : 0;
+      int tot;
+      const int ex = block_excl_scan(c, tot);
+      if (d < m2) qoff2[d] = carry + ex;
+      carry += tot;
+    }
+    if (threadIdx.x == 0) qoff2[m2] = carry;
+    for (int d = threadIdx.x; d < m2; d += blockDim.x) qcnt2[d] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      int64_t s = 0;
+      for (int o = roff[i]; o < roff[i + 1]; ++o) {
+        const int d = rr[o];
+        s += cost2[d];
+        qh2[qoff2[d] + atomicAdd(&qcnt2[d], 1)] = i;
+      }
+      marg[i] = s;
+    }
+    __syncthreads();
+    const Refs Rs{roff, nullptr, 0};
+    if (threadIdx.x < kGreedyThreads) greedy_block(n, hid, Rs, rr, cost2, k, marg, ev2, qoff2, qh2, out);
+    __syncthreads();
+  } else {
+    build_instance_index(n, R, rref, m, cost, marg_g, qoff, qcnt, qh, ev);
+    greedy_cta(n, hid_g, R, rref, cost, k, marg_g, taken_g, ev, qoff, qh, out);
+  }
+}
+
+// FIFO (reclaim.cpp:69-83): the k oldest by (mapped_at, id); rank selection.
+__device__ void fifo_core(int n, const int* hid, const int64_t* mapped, int k, int* out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t mi = mapped[i];
+    const int ii = hid[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const int64_t mj = mapped[j];
+      const int ij = hid[j];
+      rank += (mj < mi) || (mj == mi && (ij < ii || (ij == ii && j < i)));
+    }
+    if (rank < k) out[rank] = ii;
+  }
+  __syncthreads();
+}
+
+// Exhaustive oracle (reclaim.cpp:85-126), n <= 20: subsets by lexicographic rank over the
+// ascending ids; cost(S) = sum of cost[r] over requests whose handle mask meets S; the
+// first minimum in rank order wins.
+__device__ void oracle_core(int n, const int* sorted_ids, int m, const unsigned* hmask,
+                            const int64_t* cost, int k, int* out) {
+  __shared__ long long binom[21][21];
+  if (threadIdx.x == 0) {
+    for (int a = 0; a <= 20; ++a)
+      for (int b = 0; b <= 20; ++b) binom[a][b] = b == 0 ? 1 : 0;
+    for (int a = 1; a <= 20; ++a)
+      for (int b = 1; b <= a; ++b) binom[a][b] = binom[a - 1][b - 1] + binom[a - 1][b];
+  }
+  __syncthreads();
+  const long long total = binom[n][k];
+  ArgMin best{0, 0, -1};
+  for (long long rnk = threadIdx.x; rnk < total; rnk += blockDim.x) {
+    unsigned mask = 0;
+    long long rr = rnk;
+    int start = 0;
+    for (int pos = 0; pos < k; ++pos)
+      for (int c = start; c < n; ++c) {
+        const long long cnt = binom[n - c - 1][k - pos - 1];
+        if (rr < cnt) {
+          mask |= 1u << c;
+          start = c + 1;
+          break;
+        }
+        rr -= cnt;
+      }
+    int64_t c = 0;
+    for (int r = 0; r < m; ++r)
+      if (hmask[r] & mask) c += cost[r];
+    ArgMin cand{c, 0, (int)rnk};
+    if (argmin_less(cand, best)) best = cand;
+  }
+  best = block_argmin(best);
+  if (threadIdx.x == 0) {
+    long long rr = best.idx;
+    int start = 0;
+    for (int pos = 0; pos < k; ++pos)
+      for (int c = start; c < n; ++c) {
+        const long long cnt = binom[n - c - 1][k - pos - 1];
+        if (rr < cnt) {
+          out[pos] = sorted_ids[c];
+          start = c + 1;
+          break;
+        }
+        rr -= cnt;
+      }
+  }
+  __syncthreads();
+}
+
+// --------------------------------------------------------------------- apply core
+
+// apply_reclaim (memory.cpp:155-180) for ids[0..k).  Converts the valid prefix (the
+// reference mutates handle by handle and throws at the first bad one), reports the
+// invalidated pages sorted per request, and -- if the whole list was valid -- releases the
+// residual pages of every evicted request.  Writes res_* and the mirror counts.
+__device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, unsigned char* smem) {
+  __shared__ int s_bad, s_nt, s_freed;
+  if (threadIdx.x == 0) {
+    s_bad = k;
+    s_nt = 0;
+    s_freed = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const int h = ids[i];
+    bool bad = h < 0 || h >= P.H || P.hstate[h] != kOffline;
+    for (int j = 0; j < i && !bad; ++j) bad = ids[j] == h;
+    if (bad) atomicMin(&s_bad, i);
+  }
+  __syncthreads();
+  const int b = s_bad;
+  if (threadIdx.x == 0 && b < k) {
+    const int h = ids[b];
+    if (h < 0 || h >= P.H) set_err(P, kErrOutOfRange, kDetApplyRange, h);
+    else set_err(P, kErrLogic, kDetNotOffline, h);
+  }
+  // Clear the chosen handles, collecting (row, logical page, physical page, block).
+  const int64_t nslots = (int64_t)b * P.S;
+  for (int64_t idx = threadIdx.x; idx < nslots; idx += blockDim.x) {
+    const int h = ids[idx / P.S];
+    const int64_t p = (int64_t)h * P.S + idx % P.S;
+    const int row = P.slot_row[p];
+    if (row < 0) continue;
+    const int pos = atomicAdd(&s_nt, 1);
+    const int blk = P.slot_blk[p];
+    P.s_qh[pos] = row;
+    P.s_rref[pos] = (int)((int64_t)h * P.S + P.slot_lid[p]);
+    P.s_tphys[pos] = (int)p;
+    P.s_tblk[pos] = blk;
+    P.s_ev[row] = 1;
+    P.bt[(int64_t)row * P.P + blk] = P.quarantine;  // quarantine remap
+    atomicSub(&P.row_npages[row], 1);
+    P.slot_row[p] = -1;
+    P.slot_lid[p] = -1;
+    P.slot_blk[p] = -1;
+  }
+  for (int i = threadIdx.x; i < b; i += blockDim.x) {
+    const int h = ids[i];
+    P.hused[h] = 0;
+    P.hstate[h] = kOnline;
+    P.hmapped[h] = t;
+    P.res_handles[i] = h;
+  }
+  __syncthreads();
+  const int nt = s_nt;
+  // evicted rows, then their rank by request id
+  int carry = 0;
+  for (int base = 0; base < P.R; base += blockDim.x) {
+    const int r = base + threadIdx.x;
+    const int f = (r < P.R && P.s_ev[r]) ? 1 : 0;
+    int tot;
+    const int ex = block_excl_scan(f, tot);
+    if (f) {
+      P.s_evrows[carry + ex] = r;
+      P.s_ev[r] = 0;
+    }
+    carry += tot;
+  }
+  const int ne = carry;
+  __syncthreads();
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    const int row = P.s_evrows[e];
+    const int64_t req = P.row_req[row];
+    int rank = 0;
+    for (int f = 0; f < ne; ++f) rank += P.row_req[P.s_evrows[f]] < req;
+    P.s_rank[row] = rank;
+    P.res_evicted[rank] = req;
+  }
+  __syncthreads();
+  // sort key (request rank, logical page, physical page), payload = block index
+  const bool in_smem = nt <= kSmemTuples;
+  int npow = 1;
+  while (npow < nt) npow <<= 1;
+  uint64_t* key = in_smem ? reinterpret_cast<uint64_t*>(smem) : P.s_key;
+  int* pay = in_smem ? reinterpret_cast<int*>(key + npow) : P.s_pay;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    key[i] = ((uint64_t)P.s_rank[P.s_qh[i]] << 48) | ((uint64_t)(uint32_t)P.s_rref[i] << 24) |
+             (uint64_t)(uint32_t)P.s_tphys[i];
+    pay[i] = P.s_tblk[i];
+  }
+  __syncthreads();
+  block_bitonic_sort(key, pay, nt);
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    const uint64_t kv = key[i];
+    const int rank = (int)(kv >> 48);
+    P.res_pages[i] = (int64_t)((kv >> 24) & 0xffffffull);
+    P.res_phys[i] = (int)(kv & 0xffffffull);
+    P.res_blk[i] = pay[i];
+    if (i == 0 || (int)(key[i - 1] >> 48) != rank) P.res_inv_off[rank] = i;
+  }
+  if (threadIdx.x == 0) P.res_inv_off[ne] = nt;
+  __syncthreads();
+  if (b == k) {
+    // Residual pages of evicted requests are plain frees (memory.cpp:176), flattened over
+    // (row, block) so the dependent loads of all rows overlap.
+    carry = 0;
+    for (int base = 0; base < ne; base += blockDim.x) {
+      const int e = base + threadIdx.x;
+      const int c = e < ne ? P.row_nblk[P.s_evrows[e]] : 0;
+      int tot;
+      const int ex = block_excl_scan(c, tot);
+      if (e < ne) P.s_qoff[e] = carry + ex;
+      carry += tot;
+    }
+    if (threadIdx.x == 0) P.s_qoff[ne] = carry;
+    __syncthreads();
+    const int total = carry;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      int lo = 0, hi = ne - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (P.s_qoff[mid] <= idx) lo = mid;
+        else hi = mid - 1;
+      }
+      const int row = P.s_evrows[lo];
+      const int64_t bi = (int64_t)row * P.P + (idx - P.s_qoff[lo]);
+      const int p = P.bt[bi];
+      if (p < 0 || p >= P.quarantine) continue;
+      P.bt[bi] = P.quarantine;
+      if (P.slot_row[p] != row) continue;
+      P.slot_row[p] = -1;
+      P.slot_lid[p] = -1;
+      P.slot_blk[p] = -1;
+      const int h = p / P.S;
+      if (atomicSub(&P.hused[h], 1) == 1) {
+        P.hstate[h] = kFree;
+        atomicAdd(&s_freed, 1);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int e = 0; e < ne; ++e) ht_erase(P, P.row_req[P.s_evrows[e]]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    P.hdr->n_offline -= b + s_freed;
+    P.hdr->n_online += b;
+    P.hdr->n_free += s_freed;
+    P.res_counts[0] = b;
+    P.res_counts[1] = ne;
+    P.res_counts[2] = nt;
+    P.mirror->r[0] = b;
+    P.mirror->r[1] = ne;
+    P.mirror->r[2] = nt;
+  }
+}
+
+__global__ void __launch_bounds__(kNT) k_apply(PoolDev P, const int* ids, int k, int64_t t) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  op_begin(P);
+  __syncthreads();
+  apply_core(P, ids, k, t, smem);
+  publish(P);
+}
+
+// Fused reclaim (sim.cpp:936-942 in one launch): build the instance from the live slots
+// (the snapshot), select k handles with the row costs, apply.
+__global__ void __launch_bounds__(kNT) k_reclaim(PoolDev P, int k, int mode, int64_t t) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nc = (P.S + 31) >> 5;
+  op_begin(P);
+  if (threadIdx.x == 0) P.mirror->r[3] = (int64_t)globaltimer_ns();  // phase stamps (r[3..6])
+  // offline handles ascending -> index space
+  int carry = 0;
+  for (int base = 0; base < P.H; base += blockDim.x) {
+    const int h = base + threadIdx.x;
+    const int f = (h < P.H && P.hstate[h] == kOffline) ? 1 : 0;
+    int tot;
+    const int ex = block_excl_scan(f, tot);
+    if (f) {
+      P.s_hid[carry + ex] = h;
+      P.s_hmap[carry + ex] = P.hmapped[h];
+    }
+    carry += tot;
+  }
+  const int n = carry;
+  if (k > n) k = n;
+  __syncthreads();
+  // distinct resident rows per handle, stride S (warp per handle, match.any dedup)
+  for (int i = wid; i < n; i += nw) {
+    int cnt = 0;
+    VALVE_DISPATCH_NC(nc, cnt = warp_distinct_rows<NC>(P, P.s_hid[i], P.s_rref + (int64_t)i * P.S));
+    if (lane == 0) P.s_cnt[i] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) P.mirror->r[4] = (int64_t)globaltimer_ns();
+  const Refs R{nullptr, P.s_cnt, P.S};
+  if (mode == 1) {
+    fifo_core(n, P.s_hid, P.s_hmap, k, P.s_pick);
+  } else {
+    greedy_select(n, P.s_hid, R, P.s_rref, P.R, P.row_cost, k, P.s_marg, P.s_taken, P.s_ev,
+                  P.s_qoff, P.s_qcnt, P.s_qh, P.s_pick, smem);
+    for (int r = threadIdx.x; r < P.R; r += blockDim.x) P.s_ev[r] = 0;  // apply re-marks rows
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) P.mirror->r[5] = (int64_t)globaltimer_ns();
+  apply_core(P, P.s_pick, k, t, smem);
+  __syncthreads();
+  if (threadIdx.x == 0) P.mirror->r[6] = (int64_t)globaltimer_ns();
+  publish(P);
+}
+
+// ---------------------------------------------------- selection over host instances
+
+// ref request id -> index in the sorted cost keys (binary search), -1 when absent.
+__global__ void k_map_refs(const int64_t* reqs, int nnz, const int64_t* keys, int m, int* rref) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  const int64_t v = reqs[e];
+  int lo = 0, hi = m - 1, found = -1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int64_t kk = keys[mid];
+    if (kk == v) {
+      found = mid;
+      break;
+    }
+    if (kk < v) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  rref[e] = found;
+}
+
+__global__ void __launch_bounds__(kNT) k_select_instance(SelectArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_missing;
+  if (threadIdx.x == 0) s_missing = 0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < A.nnz; e += blockDim.x)
+    if (A.rref[e] < 0) s_missing = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) A.status[0] = 0;
+  // reclaim.cpp:13: cost_of throws on the first evaluation (greedy / exhaustive, k > 0);
+  // fifo never looks at costs (reclaim.cpp:69-83)
+  if (A.k > 0 && s_missing && A.mode != 1) {
+    if (threadIdx.x == 0) A.status[0] = kDetNoCost;
+    return;
+  }
+  const Refs R{A.roff, nullptr, 0};
+  if (A.mode == 0) {
+    greedy_select(A.n, A.hid, R, A.rref, A.m, A.cost, A.k, A.marg, A.taken, A.ev, A.qoff, A.qcnt,
+                  A.qh, A.out, smem);
+  } else if (A.mode == 1) {
+    fifo_core(A.n, A.hid, A.mapped, A.k, A.out);
+  } else if (A.k > 0) {
+    for (int i = threadIdx.x; i < A.n; i += blockDim.x) {
+      int rank = 0;
+      for (int j = 0; j < A.n; ++j) rank += A.hid[j] < A.hid[i] || (A.hid[j] == A.hid[i] && j < i);
+      A.taken[rank] = A.hid[i];
+      A.qcnt[i] = rank;  // position of handle i in sorted order
+    }
+    for (int r = threadIdx.x; r < A.m; r += blockDim.x) A.ev[r] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < A.n; i += blockDim.x)
+      for (int e = A.roff[i]; e < A.roff[i + 1]; ++e)
+        atomicOr(reinterpret_cast<unsigned*>(&A.ev[A.rref[e]]), 1u << A.qcnt[i]);
+    __syncthreads();
+    oracle_core(A.n, A.taken, A.m, reinterpret_cast<const unsigned*>(A.ev), A.cost, A.k, A.out);
+  }
+}
+
+// evicted_cost (reclaim.cpp:19-31): sequential union walk in one thread (it defines an
+// error order -- unknown id / missing cost -- that a parallel sum would not preserve).
+__global__ void k_evicted_cost(SelectArgs A, const int* pick, int n_pick) {
+  if (threadIdx.x != 0) return;
+  for (int r = 0; r < A.m; ++r) A.ev[r] = 0;
+  int64_t total = 0;
+  A.status[0] = 0;
+  for (int j = 0; j < n_pick; ++j) {
+    int hi = -1;
+    for (int i = 0; i < A.n; ++i)
+      if (A.hid[i] == pick[j]) {
+        hi = i;
+        break;
+      }
+    if (hi < 0) {
+      A.status[0] = kDetApplyRange;  // unknown handle id
+      return;
+    }
+    for (int e = A.roff[hi]; e < A.roff[hi + 1]; ++e) {
+      const int r = A.rref[e];
+      if (r < 0) {
+        A.status[0] = kDetNoCost;
+        return;
+      }
+      if (A.ev[r]) continue;
+      A.ev[r] = 1;
+      total += A.cost[r];
+    }
+  }
+  A.result[0] = total;
+}
+
+}  // namespace valve

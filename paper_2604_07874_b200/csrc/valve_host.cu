@@ -179,6 +179,19 @@ struct valve_pool {
   }
 };
 
+constexpr size_t kReclaimSmemBytes = 160 * 1024;  // see reclaim_kernels.cu
+
+static void set_reclaim_smem_attrs() {
+  // per device, per process (cheap to repeat)
+  ck(cudaFuncSetAttribute(k_reclaim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReclaimSmemBytes),
+     "cudaFuncSetAttribute");
+  ck(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReclaimSmemBytes),
+     "cudaFuncSetAttribute");
+  ck(cudaFuncSetAttribute(k_select_instance, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)kReclaimSmemBytes),
+     "cudaFuncSetAttribute");
+}
+
 static void pool_init(valve_pool* p, const valve_pool_config& c) {
   if (c.total_handles <= 0 || c.handle_size_pages <= 0 || c.page_size_tokens <= 0)
     fail(VALVE_INVALID_ARGUMENT, "MemoryPool: sizes must be > 0");  // memory.cpp:15
@@ -287,15 +300,11 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   ck(cudaMemcpyAsync(d.hdr, &hdr, sizeof hdr, cudaMemcpyHostToDevice, p->stream), "upload");
   ck(cudaStreamSynchronize(p->stream), "init");
   p->mirror->n_free = H;
-  // dynamic shared memory of the warp-buffer kernels
-  p->smem_snapshot = (size_t)32 * S * (8 + 4);
-  p->smem_reclaim = (size_t)32 * S * 4;
-  ck(cudaFuncSetAttribute(k_snapshot, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)std::max<size_t>(p->smem_snapshot, 1)),
-     "cudaFuncSetAttribute");
-  ck(cudaFuncSetAttribute(k_reclaim, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)std::max<size_t>(p->smem_reclaim, 1)),
-     "cudaFuncSetAttribute");
+  // dynamic shared memory: greedy marginals (2048 handles) aliased with the apply sort
+  // buffers (8192 x {u64 key, i32 block})
+  p->smem_snapshot = 0;
+  p->smem_reclaim = kReclaimSmemBytes;
+  set_reclaim_smem_attrs();
 }
 
 namespace {
@@ -498,7 +507,7 @@ int valve_pool_apply_reclaim(valve_pool* p, const int* ids, int k, int64_t t, in
     ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
     if (k) ck(cudaMemcpyAsync(p->d_ids, ids, (size_t)k * 4, cudaMemcpyHostToDevice, p->stream), "upload ids");
     try {
-      p->launch1("apply_reclaim", k_apply, 0, p->d, (const int*)p->d_ids, k, t);
+      p->launch1("apply_reclaim", k_apply, p->smem_reclaim, p->d, (const int*)p->d_ids, k, t);
     } catch (const Err&) {
       p->last_n_handles = (int)p->mirror->r[0];
       p->last_n_evicted = (int)p->mirror->r[1];
@@ -577,6 +586,18 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
     if (n_evicted) *n_evicted = p->last_n_evicted;
     if (n_pages) *n_pages = p->last_n_pages;
   });
+}
+
+int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[5]) {
+  const int64_t* r = p->mirror->r;
+  out[0] = r[4] - r[3];
+  out[1] = r[5] - r[4];
+  out[2] = r[6] - r[5];
+  long long cyc[2] = {0, 0};
+  cudaMemcpyFromSymbol(cyc, valve::g_greedy_cycles, sizeof cyc);
+  out[3] = cyc[0];
+  out[4] = cyc[1];
+  return VALVE_OK;
 }
 
 int valve_pool_last_reclaim(const valve_pool* cp, int* handles, int64_t* evicted, int* inv_off,
@@ -871,7 +892,8 @@ int valve_select(int device, int n, const int* ids, const int64_t* mapped, const
     std::lock_guard<std::mutex> lk(C.mu);
     ck(cudaSetDevice(device), "cudaSetDevice");
     SelectArgs A = upload_instance(C, n, ids, mapped, off, reqs, m, keys, vals, k, mode);
-    k_select_instance<<<1, kNT, 0, C.stream>>>(A);
+    set_reclaim_smem_attrs();
+    k_select_instance<<<1, kNT, kReclaimSmemBytes, C.stream>>>(A);
     counted();
     ck(cudaGetLastError(), "select launch");
     int status = 0;
@@ -1137,7 +1159,8 @@ int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work*
     if (n_req <= 0) return;
     cudaStream_t st = as_stream(s, p->stream);
     ck(cudaSetDevice(g->device), "cudaSetDevice");
-    const int64_t chunk = 65536;
+    const int64_t chunk = w->tile_bytes > 0 ? w->tile_bytes : 16384;
+    if (chunk % 16) fail(VALVE_INVALID_ARGUMENT, "offline_launch: tile_bytes must be a 16-byte multiple");
     const int cpp = (int)((p->d.page_bytes + chunk - 1) / chunk);
     if (n_req + 1 > g->cap_prefix) {
       if (g->d_prefix) cudaFree(g->d_prefix);

@@ -41,6 +41,7 @@ __global__ void k_select_instance(SelectArgs A);
 __global__ void k_map_refs(const int64_t* reqs, int nnz, const int64_t* keys, int m, int* rref);
 __global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix);
 __global__ void k_evicted_cost(SelectArgs A, const int* pick, int n_pick);
+extern __device__ long long g_greedy_cycles[2];
 
 // reclaim copy (copy_kernels.cu)
 struct CopyArgs {

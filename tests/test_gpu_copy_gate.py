@@ -87,7 +87,7 @@ def test_apply_reclaim_copy_matches_explicit_ids(oracle_c):
 def _offline_setup(torch, pool, reqs):
     rows = [pool.request_row(r) for r in reqs]
     npages = [pool.offline_pages_of(r) for r in reqs]
-    cpp = -(-pool.page_bytes // 65536)
+    cpp = -(-pool.page_bytes // 16384)  # default tile: 16 KiB
     total = sum(npages) * cpp
     t_rows = torch.tensor(rows, dtype=torch.int32, device="cuda")
     t_np = torch.tensor(npages, dtype=torch.int32, device="cuda")

@@ -226,8 +226,9 @@ def run_valve(args, rank, world, dist):
         nh, ne, npg = pool.reclaim(args.k, t, 0)
         e3.record(pool_stream)
         res = pool.last_reclaim()
-        cs = pool.reclaim_copy(host.ptr, host.nbytes, cp)
+        pool.reclaim_copy_start(host.ptr, host.nbytes, cp)  # copy overlaps the restore
         restore(res.evicted_requests)
+        cs = pool.reclaim_copy_wait()
         gate.release(gen[0])
         if record:
             torch.cuda.synchronize()
@@ -302,25 +303,37 @@ def run_valve(args, rank, world, dist):
 
     # ------------------------------------------------ e2e through the reference-facing API
     e2e_bytes = e2e_h2d = e2e_d2h = 0
+    brk = {"quiesce": 0.0, "snapshot": 0.0, "select": 0.0, "apply": 0.0, "restore": 0.0, "copy_wait": 0.0}
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     for _ in range(max(1, args.steps // 2)):
         gen[0] += 1
+        p0 = time.perf_counter()
         gate.launch_offline(pool, None, None, 0, 0, None, stream=off_stream.cuda_stream)
         gate.raise_(gen[0])
         gate.wait_quiesced(gen[0])
         torch.cuda.current_stream().wait_stream(gate_stream)
         torch.cuda.synchronize()
+        p1 = time.perf_counter()
         inst = pool.snapshot()                                   # D2H instance
         inst.cost = {r: live[r][1] for h in inst.handles for r in h.requests}
         nnz = sum(len(h.requests) for h in inst.handles)
+        p2 = time.perf_counter()
         ids = A.selective_reclaim(inst, args.k, device=gpu)      # H2D instance, D2H ids
         t += 10
+        p3 = time.perf_counter()
         res = pool.apply_reclaim(ids, t)                         # H2D ids, D2H result
         npg = sum(len(v) for v in res.invalidated_pages.values())
-        cs = pool.reclaim_copy(host.ptr, host.nbytes, cp)        # D2H page bytes
+        pool.reclaim_copy_start(host.ptr, host.nbytes, cp)       # D2H page bytes
+        p4 = time.perf_counter()
         restore(res.evicted_requests)
+        p5 = time.perf_counter()
+        cs = pool.reclaim_copy_wait()
         gate.release(gen[0])
+        p6 = time.perf_counter()
+        for key, a, b in (("quiesce", p0, p1), ("snapshot", p1, p2), ("select", p2, p3),
+                          ("apply", p3, p4), ("restore", p4, p5), ("copy_wait", p5, p6)):
+            brk[key] += (b - a) * 1e3
         n = len(inst.handles)
         m = len(inst.cost)
         e2e_d2h += n * 16 + 4 + nnz * 8 + 4 * len(ids) + len(res.evicted_requests) * 12 + npg * 16 + cs.bytes
@@ -390,6 +403,7 @@ def run_valve(args, rank, world, dist):
             "h2d_bytes_per_step": int(e2e_h2d / n_e2e),
             "d2h_bytes_per_step": int(e2e_d2h / n_e2e),
             "path": "snapshot() -> selective_reclaim(instance) -> apply_reclaim(ids) -> copy, host buffers",
+            "breakdown_ms_per_step": {k: round(v / max(1, args.steps // 2), 3) for k, v in brk.items()},
         },
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),

@@ -139,6 +139,12 @@ void valve_copy_params_default(valve_copy_params* c);
  * Synchronous. */
 int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
                             const valve_copy_params* params, valve_copy_stats* stats);
+/* Asynchronous form: the copy runs on the pool's copy stream, ordered after the report, while
+ * bookkeeping calls (reserve/release/grow/...) proceed on the pool stream; the next
+ * apply_reclaim / reclaim / fill_pages waits for it automatically.  One copy in flight. */
+int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_bytes,
+                                  const valve_copy_params* params);
+int valve_pool_reclaim_copy_wait(valve_pool* p, valve_copy_stats* stats);
 /* Pinned, device-mapped host staging for reclaimed pages (cudaHostAlloc, mapped). */
 int valve_host_alloc(int64_t bytes, void** out);
 void valve_host_free(void* p);

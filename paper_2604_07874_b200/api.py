@@ -658,6 +658,9 @@ def _declare_valve_extras(L):
         "valve_copy_params_default": (None, [P(CopyParams)]),
         "valve_pool_reclaim_copy": (C.c_int, [vp, vp, i64, P(CopyParams), P(CopyStats)]),
         "valve_pool_reclaim_copy_ce": (C.c_int, [vp, vp, i64, P(CopyStats)]),
+        "valve_pool_reclaim_copy_start": (C.c_int, [vp, vp, i64, P(CopyParams)]),
+        "valve_pool_reclaim_copy_wait": (C.c_int, [vp, P(CopyStats)]),
+        "valve_pool_reclaim_phases": (C.c_int, [vp, P(i64)]),
         "valve_host_alloc": (C.c_int, [i64, P(vp)]),
         "valve_host_free": (None, [vp]),
         "valve_pool_fill_pages": (C.c_int, [vp]),
@@ -739,6 +742,22 @@ class DevicePool(MemoryPool):
                 self._h, C.c_void_p(host_ptr), int(nbytes),
                 C.byref(params) if params is not None else None, C.byref(st)))
         return st
+
+    def reclaim_copy_start(self, host_ptr: int, nbytes: int, params: Optional[CopyParams] = None):
+        """Start the gather copy asynchronously (overlaps later bookkeeping calls)."""
+        self._b.check(self._b.lib.valve_pool_reclaim_copy_start(
+            self._h, C.c_void_p(host_ptr), int(nbytes), C.byref(params) if params is not None else None))
+
+    def reclaim_copy_wait(self) -> CopyStats:
+        st = CopyStats()
+        self._b.check(self._b.lib.valve_pool_reclaim_copy_wait(self._h, C.byref(st)))
+        return st
+
+    def reclaim_phases_us(self):
+        """(instance, select, apply) device microseconds of the last reclaim()."""
+        out = _arr(i64, 5)
+        self._b.check(self._b.lib.valve_pool_reclaim_phases(self._h, _ptr(out, i64)))
+        return out[0] / 1e3, out[1] / 1e3, out[2] / 1e3
 
     def view(self) -> PoolView:
         v = PoolView()

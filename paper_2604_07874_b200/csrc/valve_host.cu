@@ -121,6 +121,17 @@ struct valve_pool {
   std::vector<void*> dev_allocs;
   int last_n_handles = 0, last_n_evicted = 0, last_n_pages = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t copy_stream = nullptr;  // reclaim copies overlap pool bookkeeping
+  cudaEvent_t ev_report = nullptr;
+  unsigned long long* d_copyctr = nullptr;
+  bool copy_pending = false;
+  int64_t copy_bytes = 0, copy_pages = 0;
+
+  // Kernels that rewrite the report (apply/reclaim) or page bytes (fill) must not overtake an
+  // in-flight copy of the previous report.
+  void order_after_copy() {
+    if (ev1) ck(cudaStreamWaitEvent(stream, ev1, 0), "event wait");
+  }
 
   template <class T>
   T* dalloc(int64_t n) {
@@ -175,6 +186,8 @@ struct valve_pool {
     if (mirror) cudaFreeHost(mirror);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev_report) cudaEventDestroy(ev_report);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -183,6 +196,8 @@ constexpr size_t kReclaimSmemBytes = 160 * 1024;  // see reclaim_kernels.cu
 
 static void set_reclaim_smem_attrs() {
   // per device, per process (cheap to repeat)
+  ck(cudaFuncSetAttribute(k_reclaim_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 32768),
+     "cudaFuncSetAttribute");
   ck(cudaFuncSetAttribute(k_reclaim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReclaimSmemBytes),
      "cudaFuncSetAttribute");
   ck(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReclaimSmemBytes),
@@ -217,6 +232,8 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
   ck(cudaEventCreate(&p->ev0), "cudaEventCreate");
   ck(cudaEventCreate(&p->ev1), "cudaEventCreate");
+  ck(cudaEventCreateWithFlags(&p->ev_report, cudaEventDisableTiming), "cudaEventCreate");
+  ck(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
   const int H = p->H, S = p->S, R = p->R;
   const int64_t HS = (int64_t)H * S;
   PoolDev& d = p->d;
@@ -270,6 +287,7 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   p->d_ids = p->dalloc<int>(std::max(H, 1) * 2);
   p->d_in64 = p->dalloc<int64_t>(R);
   p->d_in64b = p->dalloc<int64_t>(R);
+  p->d_copyctr = p->dalloc<unsigned long long>(4);
   d.slot_bytes = c.slot_bytes;
   d.page_bytes = c.page_bytes;
   if (c.slot_bytes > 0) {
@@ -507,6 +525,7 @@ int valve_pool_apply_reclaim(valve_pool* p, const int* ids, int k, int64_t t, in
     ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
     if (k) ck(cudaMemcpyAsync(p->d_ids, ids, (size_t)k * 4, cudaMemcpyHostToDevice, p->stream), "upload ids");
     try {
+      p->order_after_copy();
       p->launch1("apply_reclaim", k_apply, p->smem_reclaim, p->d, (const int*)p->d_ids, k, t);
     } catch (const Err&) {
       p->last_n_handles = (int)p->mirror->r[0];
@@ -578,6 +597,7 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
     if (k < 0) fail(VALVE_INVALID_ARGUMENT, "selective_reclaim: k must be >= 0");
     if (mode != VALVE_SELECT_SELECTIVE && mode != VALVE_SELECT_FIFO)
       fail(VALVE_INVALID_ARGUMENT, "reclaim: device-fused mode must be selective or fifo");
+    p->order_after_copy();
     p->launch1("reclaim", k_reclaim, p->smem_reclaim, p->d, k, mode, t);
     p->last_n_handles = (int)p->mirror->r[0];
     p->last_n_evicted = (int)p->mirror->r[1];
@@ -614,6 +634,7 @@ int valve_pool_fill_pages(valve_pool* p) {
   return guard([&] {
     if (!p->d.pages) fail(VALVE_LOGIC_ERROR, "fill_pages: pool has no page store (slot_bytes = 0)");
     ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    p->order_after_copy();
     k_fill_pages<<<148 * 8, 256, 0, p->stream>>>(p->d);
     counted();
     p->sync_and_check("fill_pages");
@@ -642,8 +663,8 @@ void valve_copy_params_default(valve_copy_params* c) {
   c->use_tma = 0;
 }
 
-int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
-                            const valve_copy_params* prm, valve_copy_stats* st) {
+int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_bytes,
+                                  const valve_copy_params* prm) {
   return guard([&] {
     valve_copy_params c;
     valve_copy_params_default(&c);
@@ -654,6 +675,7 @@ int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
     if (!p->d.pages) fail(VALVE_LOGIC_ERROR, "reclaim_copy: pool has no page store");
     if (c.chunk_bytes % 16 || c.threads % 32 || c.threads > 512)
       fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: chunk must be a 16-byte multiple, threads <= 512");
+    if (p->copy_pending) fail(VALVE_LOGIC_ERROR, "reclaim_copy: a copy is already in flight");
     const int64_t need = (int64_t)p->last_n_pages * p->d.page_bytes;
     if (dst_bytes < need) fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: destination too small");
     if (reinterpret_cast<uintptr_t>(host_dst) % 16)
@@ -674,42 +696,57 @@ int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
     A.dst = static_cast<uint8_t*>(ddst);
     A.ns_per_byte = c.rate_bytes_per_s > 0 ? 1e9 / c.rate_bytes_per_s : 0.0;
     A.burst_bytes = c.burst_bytes;
-    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(p->d_in64);  // 3 words
-    ck(cudaMemsetAsync(ctr, 0, 24, p->stream), "memset");
+    unsigned long long* ctr = p->d_copyctr;
     A.cursor = ctr;
     A.t_first = ctr + 1;
     A.t_last = ctr + 2;
-    ck(cudaEventRecord(p->ev0, p->stream), "event");
+    // the copy runs on its own stream after the report exists; bookkeeping on the pool
+    // stream overlaps it, and the next apply/reclaim/fill waits for it (report + page bytes)
+    ck(cudaEventRecord(p->ev_report, p->stream), "event");
+    ck(cudaStreamWaitEvent(p->copy_stream, p->ev_report, 0), "event wait");
+    ck(cudaMemsetAsync(ctr, 0, 24, p->copy_stream), "memset");
+    ck(cudaEventRecord(p->ev0, p->copy_stream), "event");
     if (A.n_chunks > 0) {
       if (c.use_tma) {
-        static bool attr = false;
-        if (!attr) {
-          ck(cudaFuncSetAttribute(k_reclaim_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  2 * 32768),
-             "cudaFuncSetAttribute");
-          attr = true;
-        }
-        k_reclaim_copy_tma<<<c.ctas, 32, 2 * 32768, p->stream>>>(A);
+        k_reclaim_copy_tma<<<c.ctas, 32, 2 * 32768, p->copy_stream>>>(A);
       } else {
-        k_reclaim_copy<<<c.ctas, c.threads, 0, p->stream>>>(A);
+        k_reclaim_copy<<<c.ctas, c.threads, 0, p->copy_stream>>>(A);
       }
       counted();
     }
-    ck(cudaEventRecord(p->ev1, p->stream), "event");
+    ck(cudaEventRecord(p->ev1, p->copy_stream), "event");
     ck(cudaGetLastError(), "reclaim_copy launch");
-    ck(cudaStreamSynchronize(p->stream), "reclaim_copy");
+    p->copy_pending = true;
+    p->copy_bytes = need;
+    p->copy_pages = p->last_n_pages;
+  });
+}
+
+int valve_pool_reclaim_copy_wait(valve_pool* p, valve_copy_stats* st) {
+  return guard([&] {
+    if (!p->copy_pending) fail(VALVE_LOGIC_ERROR, "reclaim_copy_wait: no copy in flight");
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    ck(cudaEventSynchronize(p->ev1), "reclaim_copy");
+    p->copy_pending = false;
     if (st) {
       float ms = 0;
       ck(cudaEventElapsedTime(&ms, p->ev0, p->ev1), "event");
       unsigned long long t[3];
-      ck(cudaMemcpy(t, ctr, 24, cudaMemcpyDeviceToHost), "read");
-      st->bytes = need;
-      st->pages = p->last_n_pages;
+      ck(cudaMemcpy(t, p->d_copyctr, 24, cudaMemcpyDeviceToHost), "read");
+      st->bytes = p->copy_bytes;
+      st->pages = p->copy_pages;
       st->kernel_ms = ms;
       st->t_first_ns = t[1];
       st->t_last_ns = t[2];
     }
   });
+}
+
+int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
+                            const valve_copy_params* prm, valve_copy_stats* st) {
+  const int rc = valve_pool_reclaim_copy_start(p, host_dst, dst_bytes, prm);
+  if (rc != VALVE_OK) return rc;
+  return valve_pool_reclaim_copy_wait(p, st);
 }
 
 int valve_host_alloc(int64_t bytes, void** out) {
@@ -734,12 +771,26 @@ int valve_pool_reclaim_copy_ce(valve_pool* p, void* host_dst, int64_t dst_bytes,
       ck(cudaMemcpyAsync(phys.data(), p->d.res_phys, phys.size() * 4, cudaMemcpyDeviceToHost, p->stream), "read");
       ck(cudaStreamSynchronize(p->stream), "read");
     }
+    // one batched copy-engine submission (CUDA >= 12.8); per-page copies if unsupported
+    std::vector<void*> dsts(phys.size()), srcs(phys.size());
+    std::vector<size_t> sizes(phys.size(), (size_t)p->d.page_bytes);
+    for (size_t i = 0; i < phys.size(); ++i) {
+      dsts[i] = static_cast<uint8_t*>(host_dst) + i * p->d.page_bytes;
+      srcs[i] = p->d.pages + (int64_t)phys[i] * p->d.slot_bytes;
+    }
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t attr_idx = 0, fail_idx = 0;
     ck(cudaEventRecord(p->ev0, p->stream), "event");
-    for (size_t i = 0; i < phys.size(); ++i)
-      ck(cudaMemcpyAsync(static_cast<uint8_t*>(host_dst) + i * p->d.page_bytes,
-                         p->d.pages + (int64_t)phys[i] * p->d.slot_bytes, (size_t)p->d.page_bytes,
-                         cudaMemcpyDeviceToHost, p->stream),
-         "cudaMemcpyAsync");
+    bool batched = false;
+    if (!phys.empty()) {
+      batched = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), phys.size(), &attr, &attr_idx,
+                                     1, &fail_idx, p->stream) == cudaSuccess;
+      if (!batched) cudaGetLastError();
+    }
+    if (!batched)
+      for (size_t i = 0; i < phys.size(); ++i)
+        ck(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDeviceToHost, p->stream), "cudaMemcpyAsync");
     ck(cudaEventRecord(p->ev1, p->stream), "event");
     ck(cudaStreamSynchronize(p->stream), "reclaim_copy_ce");
     if (st) {

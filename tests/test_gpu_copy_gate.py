@@ -189,3 +189,22 @@ def test_quarantine_canary_catches_ungated_reclaim():
     side.synchronize()
     s = gate.read()
     assert s.canary_hits >= 1
+
+
+def test_async_copy_overlaps_bookkeeping(oracle_c):
+    """copy_start -> reserve/release calls on the pool stream -> wait: images unchanged; the
+    next reclaim waits for the copy before rewriting the report."""
+    rng = random.Random(21)
+    pool, live = _pool_with_pages(rng)
+    _, _, n_pages = pool.reclaim(4, 1000)
+    res = pool.last_reclaim()
+    buf = A.HostBuffer(n_pages * pool.page_bytes)
+    pool.reclaim_copy_start(buf.ptr, buf.nbytes, A.copy_params(ctas=2, chunk_bytes=4096,
+                                                                 rate_bytes_per_s=5e8))
+    for r in res.evicted_requests:  # re-admit while the (rate-bounded) copy still runs
+        pool.offline_reserve(r, 3, 1001)
+    pool.reclaim(2, 1002)           # must not overwrite the report under the copy
+    st = pool.reclaim_copy_wait()
+    assert st.bytes == n_pages * pool.page_bytes
+    assert np.array_equal(buf.view(), _expected_images(oracle_c, res, pool.page_bytes))
+    pool.check_invariants()

@@ -212,7 +212,8 @@ typedef struct {
   uint64_t t_quiesced_ns;
   uint64_t tiles_done;
   uint64_t canary_hits;    /* reads that resolved to the quarantine page */
-  uint64_t tiles_claimed;  /* the HBM cursor (claims, incl. one overshoot per retiring warp) */
+  uint64_t tiles_claimed;  /* tiles handed out by the HBM stripe cursors (the context save) */
+  uint64_t t_raise_ns;     /* %globaltimer of the last valve_gate_raise_stamped() */
 } valve_gate_state;
 int valve_gate_create(int device, valve_gate** out);
 void valve_gate_destroy(valve_gate* g);
@@ -220,6 +221,9 @@ void valve_gate_destroy(valve_gate* g);
  * high-priority stream).  Takes no SM: works while offline kernels occupy every SM. */
 int valve_gate_raise(valve_gate* g, uint32_t gen, void* stream);
 int valve_gate_release(valve_gate* g, uint32_t gen, void* stream);
+/* Diagnostic raise by a one-thread kernel that stamps %globaltimer (t_raise_ns) before the
+ * release-store of the gate word; needs a free SM slot, unlike valve_gate_raise. */
+int valve_gate_raise_stamped(valve_gate* g, uint32_t gen, void* stream);
 /* Makes `stream` wait (cuStreamWaitValue) until every gated kernel acknowledged `gen`. */
 int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* stream);
 /* TP fan-out: members' gate words are written by the leader over NVLink peer memory. */

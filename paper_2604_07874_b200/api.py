@@ -630,7 +630,7 @@ class GateState(C.Structure):
     _fields_ = [("gen", u32), ("closed", u32), ("quiesced_gen", u32), ("live_ctas", u32),
                 ("t_first_seen_ns", C.c_uint64), ("t_quiesced_ns", C.c_uint64),
                 ("tiles_done", C.c_uint64), ("canary_hits", C.c_uint64),
-                ("tiles_claimed", C.c_uint64)]
+                ("tiles_claimed", C.c_uint64), ("t_raise_ns", C.c_uint64)]
 
 
 class OfflineWork(C.Structure):
@@ -670,6 +670,7 @@ def _declare_valve_extras(L):
         "valve_gate_destroy": (None, [vp]),
         "valve_gate_raise": (C.c_int, [vp, u32, vp]),
         "valve_gate_release": (C.c_int, [vp, u32, vp]),
+        "valve_gate_raise_stamped": (C.c_int, [vp, u32, vp]),
         "valve_gate_wait_quiesced": (C.c_int, [vp, u32, vp]),
         "valve_gate_attach_peers": (C.c_int, [vp, P(vp), C.c_int]),
         "valve_gate_read": (C.c_int, [vp, P(GateState)]),
@@ -828,6 +829,10 @@ class Gate:
 
     def raise_(self, gen: int, stream: Optional[int] = None):
         self._b.check(self._b.lib.valve_gate_raise(self._h, gen, C.c_void_p(stream) if stream else None))
+
+    def raise_stamped(self, gen: int, stream: Optional[int] = None):
+        self._b.check(self._b.lib.valve_gate_raise_stamped(self._h, gen,
+                                                           C.c_void_p(stream) if stream else None))
 
     def release(self, gen: int, stream: Optional[int] = None):
         self._b.check(self._b.lib.valve_gate_release(self._h, gen, C.c_void_p(stream) if stream else None))

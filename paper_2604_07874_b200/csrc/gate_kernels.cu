@@ -25,6 +25,12 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   return v;
 }
 
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -61,18 +67,35 @@ __global__ void __launch_bounds__(256) k_offline_decode(OfflineArgs A) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) q[i] = 0.0625f * (float)((lane * 8 + i) % 16 - 8);
   unsigned long long done = 0;
+  const unsigned long long total = (unsigned long long)A.tile_prefix[A.n_requests];
+  const unsigned long long per = (total + kStripes - 1) / kStripes;
+  int stripe = (blockIdx.x * 7 + (threadIdx.x >> 5) * 13) % kStripes, visited = 0;  // lane 0 state
+  // The gate read for the next claim is issued at the start of the current tile (relaxed: the
+  // gate publishes no data) and consumed at its end, so its latency hides under the tile's
+  // loads; a gate raised mid-tile is therefore seen one tile late at most (quiesce <= 2 tiles).
+  unsigned gate_seen = A.poll ? ld_acquire_gpu(&A.g->closed) : 0u;
   for (;;) {
     long long tile = -1;
     if (lane == 0) {
       bool stop = false;
-      if (A.poll && ld_acquire_gpu(&A.g->closed)) {
+      if (gate_seen) {
         stop = true;
         atomicCAS(&A.g->t_first_seen, 0ull, globaltimer_ns());
       }
-      if (!stop) tile = (long long)atomicAdd(&A.g->cursor, 1ull);
+      while (!stop && visited < kStripes) {  // claim from this warp's stripe, then move on
+        const unsigned long long local = atomicAdd(&A.g->cursor[stripe], 1ull);
+        const unsigned long long t = (unsigned long long)stripe * per + local;
+        if (local < per && t < total) {
+          tile = (long long)t;
+          break;
+        }
+        stripe = (stripe + 1) % kStripes;
+        ++visited;
+      }
     }
     tile = __shfl_sync(kFull, tile, 0);
-    if (tile < 0 || tile >= A.tile_prefix[A.n_requests]) break;
+    if (tile < 0) break;
+    if (A.poll && lane == 0) gate_seen = ld_relaxed_gpu(&A.g->closed);  // consumed next round
     // locate (request, page, chunk): binary search over the tile prefix
     int lo = 0, hi = A.n_requests - 1;
     while (lo < hi) {
@@ -92,15 +115,15 @@ __global__ void __launch_bounds__(256) k_offline_decode(OfflineArgs A) {
       const int64_t len = min(A.chunk_bytes, A.page_bytes - off);
       const uint4* src = reinterpret_cast<const uint4*>(A.pages + (int64_t)phys * A.slot_bytes + off);
       const int nvec = (int)(len >> 4);
-      for (int base = 0; base < nvec; base += 32 * 4) {
-        uint4 v[4];
+      for (int base = 0; base < nvec; base += 32 * 8) {
+        uint4 v[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
           const int i = base + u * 32 + lane;
           v[u] = i < nvec ? ld_stream(src + i) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) acc += dot8(v[u], q);
+        for (int u = 0; u < 8; ++u) acc += dot8(v[u], q);
       }
     }
 #pragma unroll
@@ -120,6 +143,16 @@ __global__ void __launch_bounds__(256) k_offline_decode(OfflineArgs A) {
       __threadfence_system();
     }
   }
+}
+
+// Diagnostic raise from a one-thread kernel: stamps %globaltimer next to the gate store so the
+// device-side preempt-to-quiesce (t_quiesced - t_raise) can be split from the stream-memop and
+// event overheads.  Needs a free SM slot (the memop raise does not).
+__global__ void k_gate_raise_stamp(GateDev* g, unsigned gen) {
+  g->t_first_seen = 0;
+  g->gen = gen;
+  g->t_raise = globaltimer_ns();
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&g->closed), "r"(1u) : "memory");
 }
 
 }  // namespace valve

@@ -428,7 +428,8 @@ __global__ void k_set_costs(PoolDev P, int n, const int64_t* reqs, const int64_t
 }
 
 // tile prefix of the offline work list: prefix[i] = sum_{j<i} npages[j] * chunks_per_page
-__global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix) {
+__global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix,
+                              unsigned long long* total_out) {
   __shared__ long long s_carry;
   if (threadIdx.x == 0) s_carry = 0;
   __syncthreads();
@@ -442,7 +443,10 @@ __global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix
     if (threadIdx.x == 0) s_carry += tot;
     __syncthreads();
   }
-  if (threadIdx.x == 0) prefix[n] = s_carry * (int64_t)cpp;
+  if (threadIdx.x == 0) {
+    prefix[n] = s_carry * (int64_t)cpp;
+    if (total_out) *total_out = (unsigned long long)(s_carry * (int64_t)cpp);
+  }
 }
 
 }  // namespace valve

@@ -1126,6 +1126,16 @@ int valve_gate_raise(valve_gate* g, uint32_t gen, void* s) {
   });
 }
 
+int valve_gate_raise_stamped(valve_gate* g, uint32_t gen, void* s) {
+  return guard([&] {
+    cudaStream_t st = as_stream(s, g->stream);
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    k_gate_raise_stamp<<<1, 1, 0, st>>>(g->d, gen);
+    counted();
+    ck(cudaGetLastError(), "raise_stamped");
+  });
+}
+
 int valve_gate_release(valve_gate* g, uint32_t gen, void* s) {
   return guard([&] {
     const MemOps& op = memops();
@@ -1186,15 +1196,22 @@ int valve_gate_read(const valve_gate* g, valve_gate_state* o) {
     o->t_quiesced_ns = h.t_quiesced;
     o->tiles_done = h.tiles_done;
     o->canary_hits = h.canary;
-    o->tiles_claimed = h.cursor;
+    const unsigned long long per = (h.total + kStripes - 1) / kStripes;
+    unsigned long long claimed = 0;
+    for (int i = 0; i < kStripes; ++i) {
+      const unsigned long long len = h.total > i * per ? std::min(per, h.total - i * per) : 0;
+      claimed += std::min(h.cursor[i], len);
+    }
+    o->tiles_claimed = claimed;
+    o->t_raise_ns = h.t_raise;
   });
 }
 
 int valve_offline_reset(valve_gate* g) {
   return guard([&] {
     ck(cudaSetDevice(g->device), "cudaSetDevice");
-    ck(cudaMemsetAsync(&g->d->cursor, 0, 3 * sizeof(unsigned long long), g->stream), "memset");
-    ck(cudaMemsetAsync(&g->d->t_first_seen, 0, 2 * sizeof(unsigned long long), g->stream), "memset");
+    ck(cudaMemsetAsync(&g->d->t_first_seen, 0, 4 * sizeof(unsigned long long), g->stream), "memset");
+    ck(cudaMemsetAsync(g->d->cursor, 0, sizeof(g->d->cursor), g->stream), "memset");
     ck(cudaStreamSynchronize(g->stream), "reset");
   });
 }
@@ -1218,7 +1235,7 @@ int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work*
       g->cap_prefix = std::max<int64_t>(n_req + 1, 2 * g->cap_prefix);
       ck(cudaMalloc((void**)&g->d_prefix, g->cap_prefix * 8), "cudaMalloc");
     }
-    k_tile_prefix<<<1, kNT, 0, st>>>(npages, n_req, cpp, g->d_prefix);
+    k_tile_prefix<<<1, kNT, 0, st>>>(npages, n_req, cpp, g->d_prefix, &g->d->total);
     counted();
     int threads = w->threads > 0 ? w->threads : 256;
     int ctas = w->ctas;
@@ -1226,7 +1243,9 @@ int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work*
       int per_sm = 0, sms = 0;
       ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_offline_decode, threads, 0), "occupancy");
       ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device), "attr");
-      ctas = per_sm * sms;
+      // 16 warps per SM with 8 x 16 B loads in flight per lane saturate HBM; more warps only
+      // stretch each tile (quiesce = one tile) without adding bandwidth
+      ctas = std::min(per_sm, std::max(1, 512 / threads)) * sms;
     }
     // never start tiles into a closed gate; count the CTAs before they can retire
     cu_ck(op.wait32((CUstream)st, dptr(&g->d->closed), 0, CU_STREAM_WAIT_VALUE_EQ), "cuStreamWaitValue32");

@@ -39,7 +39,8 @@ __global__ void k_fill_pages(PoolDev P);
 __global__ void k_set_costs(PoolDev P, int n, const int64_t* reqs, const int64_t* costs);
 __global__ void k_select_instance(SelectArgs A);
 __global__ void k_map_refs(const int64_t* reqs, int nnz, const int64_t* keys, int m, int* rref);
-__global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix);
+__global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix,
+                              unsigned long long* total_out);
 __global__ void k_evicted_cost(SelectArgs A, const int* pick, int n_pick);
 extern __device__ long long g_greedy_cycles[2];
 
@@ -61,6 +62,9 @@ __global__ void k_reclaim_copy(CopyArgs A);
 __global__ void k_reclaim_copy_tma(CopyArgs A);
 
 // gate (gate_kernels.cu)
+// The tile space of a work list is split into kStripes contiguous stripes, each with its own
+// claim cursor (a single cursor saturates one L2 atomic unit at ~9k claiming warps).
+constexpr int kStripes = 64;
 struct GateDev {
   unsigned int closed;        // polled word
   unsigned int gen;
@@ -68,10 +72,13 @@ struct GateDev {
   unsigned int quiesced_gen;
   unsigned long long t_first_seen;
   unsigned long long t_quiesced;
-  unsigned long long cursor;  // tiles claimed (== done once quiesced)
   unsigned long long tiles_done;
   unsigned long long canary;
+  unsigned long long total;               // tiles of the current work list
+  unsigned long long cursor[kStripes];    // per-stripe claims (the context save)
+  unsigned long long t_raise;             // %globaltimer of a kernel-issued raise (diagnostic)
 };
+__global__ void k_gate_raise_stamp(GateDev* g, unsigned gen);
 struct OfflineArgs {
   GateDev* g;
   const uint8_t* pages;

@@ -1,0 +1,508 @@
+"""Real-time colocation loop on one B200: measured online TTFT/TPOT deltas.
+
+A thin runtime around the product kernels, following the reference simulator's online/offline
+engines (sim.cpp:391-858) but in wall-clock time on the device:
+
+* online: a random-init Llama-3-8B-shaped decoder in PyTorch (bf16, cuBLAS GEMMs, SDPA
+  attention; never gated -- it is the latency-critical tenant).  Prefill emits no token; a
+  decode iteration emits one token for every decoding request (sim.cpp:625-719).
+* offline: the gated tile-looped kernel over the pool's offline KV pages
+  (valve_offline_launch), running whenever the ChannelController is Enabled.
+* lane edges drive the host ChannelController (channel.cpp), bound to the HBM gate: the busy
+  edge raises the gate and the online stream waits (cuStreamWaitValue) for every offline CTA to
+  retire before its first kernel; idle edge -> cooldown T_cool = 2G -> enable -> gate released ->
+  offline relaunched from its HBM cursor.
+* online KV pages are charged against the reservation on the device pool (MemoryPool API):
+  free handles first, otherwise a fused device reclaim of k offline handles (Algorithm 1 +
+  apply_reclaim) whose evicted requests are re-admitted later -- sim.cpp:469-556.
+
+The same online trace is run standalone (no offline tenant, no gate) and colocated; the deltas
+are the reference's paired per-request increases (metrics.cpp:49-65, 231-241).
+"""
+from __future__ import annotations
+
+import heapq
+import math
+import random
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import torch
+import torch.nn.functional as F
+
+from . import api as A
+
+
+# ------------------------------------------------------------------------- online model
+
+@dataclass
+class ModelShape:
+    """Llama-3-8B: 32 layers, d 4096, GQA 32/8 heads x 128, MLP 14336, vocab 128256."""
+    layers: int = 32
+    d: int = 4096
+    heads: int = 32
+    kv_heads: int = 8
+    head_dim: int = 128
+    ffn: int = 14336
+    vocab: int = 128256
+
+
+class OnlineModel:
+    """Random-init (N(0, 0.02), bf16) decoder.  KV lives in per-layer slot tensors
+    [slots, kv_heads, max_tokens, head_dim]; prefill uses SDPA (causal, flash-eligible),
+    decode attends the whole batch at once with a length mask."""
+
+    def __init__(self, shape: ModelShape, device, seed: int = 0, slots: int = 16, max_tokens: int = 4352):
+        g = torch.Generator(device=device).manual_seed(seed)
+        s = shape
+        self.s = s
+        dt = torch.bfloat16
+
+        def w(*shape_):
+            return (torch.randn(*shape_, generator=g, device=device, dtype=torch.float32) * 0.02).to(dt)
+
+        qkv = (s.heads + 2 * s.kv_heads) * s.head_dim
+        self.layers = [dict(wqkv=w(s.d, qkv), wo=w(s.heads * s.head_dim, s.d), w13=w(s.d, 2 * s.ffn),
+                            w2=w(s.ffn, s.d)) for _ in range(s.layers)]
+        self.emb = w(s.vocab, s.d)
+        self.lm = w(s.d, s.vocab)
+        self.device = device
+        self.max_tokens = max_tokens
+        self.K = [torch.zeros(slots, s.kv_heads, max_tokens, s.head_dim, device=device, dtype=dt)
+                  for _ in range(s.layers)]
+        self.V = [torch.zeros_like(k) for k in self.K]
+        self.free_slots = list(range(slots))
+
+    @staticmethod
+    def _rms(x):
+        return x * torch.rsqrt(x.float().pow(2).mean(-1, keepdim=True) + 1e-5).to(x.dtype)
+
+    def _qkv(self, L, x):
+        s = self.s
+        h = self._rms(x) @ L["wqkv"]
+        return h.split([s.heads * s.head_dim, s.kv_heads * s.head_dim, s.kv_heads * s.head_dim], -1)
+
+    def _mlp(self, L, x, a):
+        x = x + a @ L["wo"]
+        g1, g3 = (self._rms(x) @ L["w13"]).chunk(2, -1)
+        return x + (F.silu(g1) * g3) @ L["w2"]
+
+    def alloc(self):
+        return self.free_slots.pop()
+
+    def free(self, slot):
+        self.free_slots.append(slot)
+
+    @torch.no_grad()
+    def prefill(self, tokens, slot):
+        s = self.s
+        T = tokens.shape[0]
+        rep = s.heads // s.kv_heads
+        x = self.emb[tokens]
+        for li, L in enumerate(self.layers):
+            q, k, v = self._qkv(L, x)
+            kh = k.view(T, s.kv_heads, s.head_dim).transpose(0, 1)
+            vh = v.view(T, s.kv_heads, s.head_dim).transpose(0, 1)
+            self.K[li][slot, :, :T] = kh
+            self.V[li][slot, :, :T] = vh
+            qh = q.view(T, s.heads, s.head_dim).transpose(0, 1).unsqueeze(0)
+            o = F.scaled_dot_product_attention(qh, kh.repeat_interleave(rep, 0).unsqueeze(0),
+                                               vh.repeat_interleave(rep, 0).unsqueeze(0), is_causal=True)
+            x = self._mlp(L, x, o[0].transpose(0, 1).reshape(T, -1))
+        return (self._rms(x[-1:]) @ self.lm).argmax(-1)
+
+    @torch.no_grad()
+    def decode(self, tokens, slots, lens):
+        s = self.s
+        B = tokens.shape[0]
+        rep = s.heads // s.kv_heads
+        idx = torch.tensor(slots, device=self.device)
+        pos = torch.tensor(lens, device=self.device)
+        n = max(lens) + 1
+        mask = torch.arange(n, device=self.device)[None, :] <= pos[:, None]  # (B, n)
+        bias = torch.zeros(B, 1, 1, n, device=self.device, dtype=torch.float32)
+        bias.masked_fill_(~mask[:, None, None, :], float("-inf"))
+        scale = 1.0 / math.sqrt(s.head_dim)
+        x = self.emb[tokens]
+        for li, L in enumerate(self.layers):
+            q, k, v = self._qkv(L, x)
+            self.K[li][idx, :, pos] = k.view(B, s.kv_heads, s.head_dim)
+            self.V[li][idx, :, pos] = v.view(B, s.kv_heads, s.head_dim)
+            Kb = self.K[li][idx, :, :n]  # (B, G, n, D)
+            Vb = self.V[li][idx, :, :n]
+            qg = q.view(B, s.kv_heads, rep, s.head_dim)
+            sc = torch.matmul(qg, Kb.transpose(-1, -2)).float() * scale + bias
+            a = torch.matmul(sc.softmax(-1).to(Vb.dtype), Vb)  # (B, G, rep, D)
+            x = self._mlp(L, x, a.reshape(B, -1))
+        return (self._rms(x) @ self.lm).argmax(-1)
+
+
+# ------------------------------------------------------------------------------ trace
+
+@dataclass
+class OnlineReq:
+    rid: int
+    arrival_us: int
+    prompt: int
+    output: int
+    first_us: int = -1
+    emits: List[int] = field(default_factory=list)
+    pages: int = 0
+
+
+def spike_trace(seed: int, horizon_s: float, base_rate: float, spike_rate: float, period_s: float,
+                width_s: float, prompt=(2000, 4000), output=(32, 128)) -> List[OnlineReq]:
+    """Poisson arrivals at base_rate, spike_rate inside [k*period, k*period + width)
+    (the reference's 'spike' generator shape, trace.cpp:131-183)."""
+    rng = random.Random(seed)
+    out, t, rid = [], 0.0, 0
+    while True:
+        in_spike = (t % period_s) < width_s
+        rate = spike_rate if in_spike else base_rate
+        t += rng.expovariate(rate)
+        if t >= horizon_s:
+            break
+        out.append(OnlineReq(rid, int(t * 1e6), rng.randint(*prompt), rng.randint(*output)))
+        rid += 1
+    return out
+
+
+# ------------------------------------------------------------------------- the runtime
+
+@dataclass
+class RunResult:
+    ttft_us: Dict[int, float]
+    tpot_us: Dict[int, float]
+    wall_s: float
+    disables: int = 0
+    reclaims: int = 0
+    reclaimed_handles: int = 0
+    offline_tiles: int = 0
+    offline_bytes: float = 0.0
+    quiesce_wait_us: List[float] = field(default_factory=list)
+    decode_iter_us: List[float] = field(default_factory=list)
+    prefill_us: List[float] = field(default_factory=list)
+
+
+class Colocation:
+    def __init__(self, model: OnlineModel, pool: Optional[A.DevicePool], gate: Optional[A.Gate],
+                 page_tokens: int = 16, max_gap_us: int = 300, resparams: Optional[A.ReservationParams] = None,
+                 tile_bytes: int = 16384, offline_ctas: int = 0):
+        self.model, self.pool, self.gate = model, pool, gate
+        self.page_tokens = page_tokens
+        self.tile_bytes = tile_bytes
+        self.offline_ctas = offline_ctas  # 0 = library default (2 CTAs of 8 warps per SM)
+        self.colocated = pool is not None
+        self.online_stream = torch.cuda.current_stream()
+        self.off_stream = torch.cuda.Stream()
+        self.resctl = A.ReservationController(resparams) if self.colocated else None
+        self.timers: list = []
+        self.seq = 0
+        self.offline_running = False
+        if self.colocated:
+            hooks = A.Hooks(schedule=self._schedule, on_disabled=lambda t: None,
+                            on_enabled=self._on_enabled, log=None)
+            # real time: the device gate takes effect at issue; its quiesce is waited on the
+            # online stream, so the modelled toggle latency is 0 (channel.cpp:13-20)
+            self.channel = A.ChannelController(0, A.CooldownPolicy(max_gap_us).cooldown_us(), hooks, gate=gate)
+
+    # timers (the channel's schedule hook, in run microseconds)
+    def _schedule(self, when, gen, cooldown):
+        heapq.heappush(self.timers, (when, self.seq, cooldown, gen))
+        self.seq += 1
+
+    def _fire_timers(self, now):
+        while self.timers and self.timers[0][0] <= now:
+            when, _, cd, gen = heapq.heappop(self.timers)
+            (self.channel.handle_cooldown if cd else self.channel.handle_toggle)(when, gen)
+
+    def _on_enabled(self, t):
+        self._launch_offline()
+
+    def _launch_offline(self):
+        if not self.colocated:
+            return
+        st = self.gate.read()
+        total = self._offline_tiles_total()
+        if total and st.tiles_claimed >= total:  # work list exhausted: start another pass
+            self._harvest += st.tiles_done
+            self.gate.reset_work()
+        self.gate.launch_offline(self.pool, None, None, 0, 0, None, stream=self.off_stream.cuda_stream,
+                                 tile_bytes=self.tile_bytes, ctas=self.offline_ctas)
+
+    def _offline_tiles_total(self):
+        return self._off_pages * (-(-self.pool.page_bytes // self.tile_bytes)) if self.colocated else 0
+
+    # ------------------------------------------------------------------ memory (sim.cpp)
+    def _acquire_online_pages(self, need, now):
+        """sim.cpp:469-511 + 535-556: reservation growth from free handles, then a fused
+        device reclaim for the shortfall; pressure growth after the charge."""
+        P = self.pool
+        hsz = P.handle_size_pages()
+        deficit = P.online_used_pages() + need - P.online_capacity_pages()
+        if deficit > 0:
+            k = -(-deficit // hsz)
+            from_free = min(k, P.free_handles())
+            if from_free:
+                P.online_grow(from_free, now)
+            deficit -= from_free * hsz
+        if deficit > 0:
+            self.resctl.record_pressure(now)
+            k = min(-(-deficit // hsz), P.offline_handles())
+            if k:
+                self._reclaim(k, now)
+        P.online_use_pages(need)
+        cap = P.online_capacity_pages()
+        if cap and P.online_used_pages() / cap >= self.resctl.params().pressure_threshold:
+            self.resctl.record_pressure(now)
+            h = P.online_handles()
+            want = self.resctl.grow_target(h, P.total_handles()) - h
+            from_free = min(max(want, 0), P.free_handles())
+            if from_free:
+                P.online_grow(from_free, now)
+            want -= from_free
+            if want > 0 and P.offline_handles():
+                self._reclaim(min(want, P.offline_handles()), now)
+
+    def _reclaim(self, k, now):
+        nh, ne, npg = self.pool.reclaim(k, now)
+        res = self.pool.last_reclaim()
+        self.res.reclaims += 1
+        self.res.reclaimed_handles += nh
+        for r in res.evicted_requests:  # evicted-waiting -> re-admitted when memory frees
+            self._evicted.append(r)
+            self._off_pages -= self._off_live.pop(r, 0)
+
+    def _readmit_offline(self, now):
+        """sim.cpp:730-753 admit_offline: resume evicted requests first."""
+        P = self.pool
+        while self._evicted:
+            r = self._evicted[0]
+            pages = self._off_req_pages[r]
+            if not P.offline_reserve(r, pages, now):
+                break
+            self._evicted.pop(0)
+            self._off_live[r] = pages
+            self._off_pages += pages
+        if self._off_live:
+            P.set_costs({r: self._off_cost[r] for r in self._off_live})
+
+    # ------------------------------------------------------------------------ main loop
+    def run(self, trace: List[OnlineReq], offline_reqs=(), horizon_s: float = 30.0) -> RunResult:
+        m = self.model
+        self.res = RunResult({}, {}, 0.0)
+        self._evicted, self._off_live, self._off_req_pages, self._off_cost = [], {}, {}, {}
+        self._off_pages = 0
+        self._harvest = 0
+        reqs = [OnlineReq(r.rid, r.arrival_us, r.prompt, r.output) for r in trace]
+        if self.colocated:
+            P = self.pool
+            P.online_grow(-(-P.total_handles() // 10), 0)
+            for rid, pages, cost in offline_reqs:
+                self._off_req_pages[rid] = pages
+                self._off_cost[rid] = cost
+                if P.offline_reserve(rid, pages, 0):
+                    self._off_live[rid] = pages
+                    self._off_pages += pages
+            P.set_costs({r: self._off_cost[r] for r in self._off_live})
+            P.fill_pages()
+            self.gate.reset_work()
+            self._launch_offline()
+        queue: List[OnlineReq] = []
+        decoding: List[OnlineReq] = []
+        caches: Dict[int, int] = {}  # request -> KV slot
+        lens: Dict[int, int] = {}
+        nxt = 0
+        busy = False
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        now_us = lambda: int((time.perf_counter() - t0) * 1e6)  # noqa: E731
+        while True:
+            now = now_us()
+            if now > horizon_s * 1e6:
+                break
+            if self.colocated:
+                self._fire_timers(now)
+            while nxt < len(reqs) and reqs[nxt].arrival_us <= now:
+                queue.append(reqs[nxt])
+                nxt += 1
+            if not queue and not decoding:
+                if busy:  # idle edge (sim.cpp:371-380)
+                    busy = False
+                    if self.colocated:
+                        self.channel.note_all_idle(now)
+                        self._readmit_offline(now)
+                if nxt >= len(reqs):
+                    break
+                if self.colocated and self.channel.offline_compute_allowed():
+                    # the offline engine's next iteration: a pass over its KV finished -> relaunch
+                    if self.gate.read().live_ctas == 0:
+                        self._launch_offline()
+                time.sleep(50e-6)
+                continue
+            if not busy:  # busy edge: raise + wait for the offline CTAs to retire (sim.cpp:362-369)
+                busy = True
+                if self.colocated:
+                    self.channel.note_busy(now)
+                    self._fire_timers(now)
+                    self.gate.wait_quiesced(self.channel.disables_issued(), self.online_stream.cuda_stream)
+                    self.res.disables = self.channel.disables_issued()
+            if queue:  # prefill the queue head
+                r = queue.pop(0)
+                need = -(-r.prompt // self.page_tokens)
+                if self.colocated:
+                    self._acquire_online_pages(need, now)
+                r.pages = need
+                caches[r.rid] = m.alloc()
+                toks = torch.randint(0, m.s.vocab, (r.prompt,), device=m.device)
+                t_it = now_us()
+                m.prefill(toks, caches[r.rid])
+                lens[r.rid] = r.prompt
+                torch.cuda.synchronize()
+                self.res.prefill_us.append(now_us() - t_it)
+                decoding.append(r)
+                continue
+            # one decode iteration over the batch
+            need_by = []
+            for r in decoding:
+                tok_after = r.prompt + len(r.emits) + 1
+                need_by.append(max(0, -(-tok_after // self.page_tokens) - r.pages))
+            if self.colocated and sum(need_by):
+                self._acquire_online_pages(sum(need_by), now)
+            for r, nb in zip(decoding, need_by):
+                r.pages += nb
+            toks = torch.randint(0, m.s.vocab, (len(decoding),), device=m.device)
+            t_it = now_us()
+            m.decode(toks, [caches[r.rid] for r in decoding], [lens[r.rid] for r in decoding])
+            torch.cuda.synchronize()
+            t_emit = now_us()
+            self.res.decode_iter_us.append(t_emit - t_it)
+            done = []
+            for r in decoding:
+                lens[r.rid] += 1
+                r.emits.append(t_emit)
+                if len(r.emits) == 1:
+                    r.first_us = t_emit
+                if len(r.emits) == r.output:
+                    done.append(r)
+            for r in done:
+                decoding.remove(r)
+                m.free(caches.pop(r.rid))
+                if self.colocated:
+                    self.pool.online_free_pages(r.pages)
+                if r.output > 1:
+                    self.res.tpot_us[r.rid] = (r.emits[-1] - r.emits[0]) / (r.output - 1)
+                self.res.ttft_us[r.rid] = r.first_us - r.arrival_us
+        torch.cuda.synchronize()
+        self.res.wall_s = time.perf_counter() - t0
+        if self.colocated:
+            gen = self.channel.disables_issued() + 1000
+            self.gate.raise_(gen)
+            self.gate.wait_quiesced(gen)
+            torch.cuda.synchronize()
+            self.res.offline_tiles = self._harvest + self.gate.read().tiles_done
+            self.res.offline_bytes = self.res.offline_tiles * self.tile_bytes
+            self.gate.release(gen)
+            torch.cuda.synchronize()
+        return self.res
+
+
+def paired_increase(base: Dict[int, float], other: Dict[int, float]):
+    """metrics.cpp:49-65: mean and max of per-request % increases over paired requests."""
+    pcts = [(other[i] - b) / b * 100.0 for i, b in sorted(base.items()) if i in other and b > 0]
+    if not pcts:
+        return {"mean_pct": None, "max_pct": None, "pairs": 0}
+    return {"mean_pct": sum(pcts) / len(pcts), "max_pct": max(pcts), "pairs": len(pcts)}
+
+
+def offline_population(seed: int, n: int, page_tokens: int = 16):
+    """Qwen2-7B offline requests: prompt 2000-4000, output 100-200."""
+    rng = random.Random(seed)
+    out = []
+    for r in range(n):
+        inp, outp = rng.randint(2000, 4000), rng.randint(100, 200)
+        out.append((r, math.ceil((inp + outp) / page_tokens), inp + rng.randint(0, outp)))
+    return out
+
+
+def warm_shapes(model: OnlineModel, trace: List[OnlineReq]):
+    """Run every prefill length and a spread of decode shapes of the trace once, so neither
+    measured run pays first-use costs (cuBLAS heuristics, allocator growth)."""
+    slot = model.alloc()
+    for r in trace:
+        model.prefill(torch.randint(0, model.s.vocab, (r.prompt,), device=model.device), slot)
+    lens = [r.prompt for r in trace[:4]]
+    for b in range(1, min(4, len(trace)) + 1):
+        for extra in range(0, 16, 4):
+            model.decode(torch.zeros(b, dtype=torch.long, device=model.device), [slot] * b,
+                         [n + extra for n in lens[:b]])
+    model.free(slot)
+    torch.cuda.synchronize()
+
+
+def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, handles=256, seed=2604,
+                   output=(8, 12), prompt=(2500, 3500), layers=32, device=0, offline_ctas=0):
+    """Paired standalone vs colocated run of one online trace (default: the pair_06 shape --
+    spike base 0.3/s, 6/s for 1 s every 8 s, prompt 2500-3500, output 8-12 -- so the online
+    lane goes idle and the offline tenant harvests the gaps).  Returns the reference's paired
+    TTFT/TPOT increases (metrics.cpp:49-65) plus harvest statistics."""
+    dev = torch.device("cuda", device)
+    model = OnlineModel(ModelShape(layers=layers), dev)
+    trace = spike_trace(seed, horizon, base, spike, period, width, prompt=prompt, output=output)
+    warm_shapes(model, trace)
+    # A/B/A: standalone, colocated, standalone.  The colocated run is paired against the
+    # per-request mean of the two standalone runs (cancels clock/thermal drift), and the two
+    # standalone runs against each other give the A/A noise floor of the same statistic.
+    solo1 = Colocation(model, None, None).run(trace, horizon_s=horizon + 30)
+    pool = A.DevicePool(handles, 64, 16, device=device, slot_bytes=2 << 20, page_bytes=917504,
+                        max_requests=4096, max_pages_per_request=1024)
+    gate = A.Gate(device)
+    colo_rt = Colocation(model, pool, gate, offline_ctas=offline_ctas)
+    colo = colo_rt.run(trace, offline_population(seed, 4 * handles), horizon_s=horizon + 30)
+    solo2 = Colocation(model, None, None).run(trace, horizon_s=horizon + 30)
+
+    def avg(d1, d2):
+        return {k: (d1[k] + d2[k]) / 2 for k in d1 if k in d2}
+
+    base_ttft, base_tpot = avg(solo1.ttft_us, solo2.ttft_us), avg(solo1.tpot_us, solo2.tpot_us)
+    ttft = paired_increase(base_ttft, colo.ttft_us)
+    tpot = paired_increase(base_tpot, colo.tpot_us)
+    aa_ttft = paired_increase(solo1.ttft_us, solo2.ttft_us)
+    aa_tpot = paired_increase(solo1.tpot_us, solo2.tpot_us)
+
+    def mean(d):
+        return sum(d.values()) / max(1, len(d))
+
+    out = {
+        "trace": {"horizon_s": horizon, "online_requests": len(trace), "base_rate": base, "spike_rate": spike,
+                  "period_s": period, "width_s": width, "prompt": list(prompt), "output": list(output),
+                  "model": f"Llama-3-8B-shaped, {layers} layers, random init bf16"},
+        "design": "A/B/A: colocated paired against the per-request mean of two standalone runs",
+        "ttft_delta_pct": ttft["mean_pct"], "ttft_delta_max_pct": ttft["max_pct"],
+        "tpot_delta_pct": tpot["mean_pct"], "tpot_delta_max_pct": tpot["max_pct"], "pairs": ttft["pairs"],
+        "aa_noise_ttft_pct": aa_ttft["mean_pct"], "aa_noise_tpot_pct": aa_tpot["mean_pct"],
+        "ttft_ms": {"standalone": mean(base_ttft) / 1e3, "colocated": mean(colo.ttft_us) / 1e3},
+        "tpot_ms": {"standalone": mean(base_tpot) / 1e3, "colocated": mean(colo.tpot_us) / 1e3},
+        "disables": colo.disables, "disables_per_request": colo.disables / max(1, len(trace)),
+        "reclaims": colo.reclaims, "reclaimed_handles": colo.reclaimed_handles,
+        "offline_ctas": offline_ctas or "default",
+        "offline_gbs_harvested": colo.offline_bytes / colo.wall_s / 1e9,
+        "prefill_ms_median": {"standalone": _median(solo1.prefill_us + solo2.prefill_us) / 1e3,
+                              "colocated": _median(colo.prefill_us) / 1e3},
+        "decode_iter_ms_median": {"standalone": _median(solo1.decode_iter_us + solo2.decode_iter_us) / 1e3,
+                                  "colocated": _median(colo.decode_iter_us) / 1e3},
+        "wall_s": {"standalone": solo1.wall_s, "colocated": colo.wall_s},
+    }
+    import gc
+
+    del pool, gate, model, colo_rt
+    gc.collect()  # the channel's ctypes hooks close over the runtime: break the cycle now
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
+
+
+def _median(xs):
+    xs = sorted(xs)
+    return xs[len(xs) // 2] if xs else float("nan")

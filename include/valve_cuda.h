@@ -228,6 +228,11 @@ int valve_gate_raise_stamped(valve_gate* g, uint32_t gen, void* stream);
 int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* stream);
 /* TP fan-out: members' gate words are written by the leader over NVLink peer memory. */
 int valve_gate_attach_peers(valve_gate* leader, valve_gate** members, int n);
+/* One process per GPU: a member exports its gate words (CUDA IPC, 64-byte handle) and the
+ * leader opens them as a remote gate (no kernels, words only) to pass to attach_peers. */
+#define VALVE_GATE_HANDLE_BYTES 64
+int valve_gate_export(const valve_gate* g, void* handle_out);
+int valve_gate_open_remote(int device, const void* handle, valve_gate** out);
 int valve_gate_read(const valve_gate* g, valve_gate_state* out);
 void* valve_gate_stream(const valve_gate* g);
 

@@ -673,6 +673,8 @@ def _declare_valve_extras(L):
         "valve_gate_raise_stamped": (C.c_int, [vp, u32, vp]),
         "valve_gate_wait_quiesced": (C.c_int, [vp, u32, vp]),
         "valve_gate_attach_peers": (C.c_int, [vp, P(vp), C.c_int]),
+        "valve_gate_export": (C.c_int, [vp, C.c_char_p]),
+        "valve_gate_open_remote": (C.c_int, [C.c_int, C.c_char_p, P(vp)]),
         "valve_gate_read": (C.c_int, [vp, P(GateState)]),
         "valve_gate_stream": (vp, [vp]),
         "valve_offline_launch": (C.c_int, [vp, vp, P(OfflineWork), vp]),
@@ -808,10 +810,33 @@ def copy_params(**kw) -> CopyParams:
 class Gate:
     """Device preemption gate (valve_gate_*)."""
 
-    def __init__(self, device: int = 0):
+    HANDLE_BYTES = 64
+
+    def __init__(self, device: int = 0, _remote_handle: Optional[bytes] = None):
         self._b = valve_backend()
         self._h = C.c_void_p()
-        self._b.check(self._b.lib.valve_gate_create(device, C.byref(self._h)))
+        self.device = device
+        self._peers = []
+        if _remote_handle is not None:
+            self._b.check(self._b.lib.valve_gate_open_remote(device, _remote_handle, C.byref(self._h)))
+        else:
+            self._b.check(self._b.lib.valve_gate_create(device, C.byref(self._h)))
+
+    @classmethod
+    def open_remote(cls, handle: bytes, device: int = 0) -> "Gate":
+        """A TP member's gate words exported by another process (CUDA IPC)."""
+        return cls(device, _remote_handle=bytes(handle))
+
+    def export(self) -> bytes:
+        buf = C.create_string_buffer(self.HANDLE_BYTES)
+        self._b.check(self._b.lib.valve_gate_export(self._h, buf))
+        return buf.raw
+
+    def attach_peers(self, members: Sequence["Gate"]):
+        """TP fan-out: raise/release/wait on this (leader) gate also drive the members' words."""
+        arr = (C.c_void_p * max(1, len(members)))(*[m.handle.value for m in members])
+        self._b.check(self._b.lib.valve_gate_attach_peers(self._h, arr, len(members)))
+        self._peers.extend(members)  # keep the member objects alive
 
     def __del__(self):
         h = getattr(self, "_h", None)

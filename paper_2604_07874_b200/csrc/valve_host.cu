@@ -1068,9 +1068,11 @@ struct valve_gate {
   std::vector<valve_gate*> peers;
   int64_t* d_prefix = nullptr;
   int64_t cap_prefix = 0;
+  bool remote = false;  // words opened from another process (CUDA IPC): no stream, no kernels
   ~valve_gate() {
     if (stream) cudaStreamSynchronize(stream);
-    if (d) cudaFree(d);
+    if (d && remote) cudaIpcCloseMemHandle(d);
+    else if (d) cudaFree(d);
     if (d_prefix) cudaFree(d_prefix);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -1162,6 +1164,42 @@ int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* s) {
             "cuStreamWaitValue32");
       cu_ck(op.write32((CUstream)st, dptr(&x->d->quiesced_gen), gen, 0), "cuStreamWriteValue32");
     }
+  });
+}
+
+int valve_gate_export(const valve_gate* g, void* handle_out) {
+  return guard([&] {
+    if (g->remote) fail(VALVE_LOGIC_ERROR, "gate_export: a remote gate cannot be re-exported");
+    static_assert(sizeof(cudaIpcMemHandle_t) <= VALVE_GATE_HANDLE_BYTES, "handle size");
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, g->d), "cudaIpcGetMemHandle");
+    std::memset(handle_out, 0, VALVE_GATE_HANDLE_BYTES);
+    std::memcpy(handle_out, &h, sizeof h);
+  });
+}
+
+int valve_gate_open_remote(int device, const void* handle, valve_gate** out) {
+  return guard([&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0)
+      fail(VALVE_CUDA_ERROR, "no CUDA device: the gate lives in HBM");
+    memops();
+    auto* g = new valve_gate;
+    g->device = device;
+    g->remote = true;
+    try {
+      ck(cudaSetDevice(device), "cudaSetDevice");
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handle, sizeof h);
+      void* p = nullptr;
+      ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      g->d = static_cast<GateDev*>(p);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
   });
 }
 

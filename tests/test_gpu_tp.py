@@ -1,0 +1,97 @@
+"""TP-group gate fan-out across processes, on one GPU: two processes (a TP group
+of 2) share cuda:0; the member's gate words are opened by the leader through CUDA IPC and
+driven with stream memory operations.  The member's gated offline kernel must quiesce on the
+leader's raise (leader waits on the member's live_ctas), keep its context (cursor), and resume
+to completion after the leader's release -- every tile exactly once."""
+import os
+import socket
+import time
+
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_07874_b200 import api as A
+    from paper_2604_07874_b200 import tp as TP
+
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    torch.cuda.set_device(0)
+    gate = A.Gate(0)
+    group = TP.TPGate(gate, rank, 2, 2, dist, opener=lambda h: A.Gate.open_remote(h, 0))
+    out = {"rank": rank}
+    if rank == 1:  # member: a long offline pass over its own pool
+        pool = A.DevicePool(64, 16, 16, slot_bytes=1 << 20, page_bytes=917504)
+        for r in range(64):
+            pool.offline_reserve(r, 16, 0)
+        pool.fill_pages()
+        gate.reset_work()
+        s = torch.cuda.Stream()
+        gate.launch_offline(pool, None, None, 0, 0, None, ctas=8, stream=s.cuda_stream)
+        dist.barrier()  # 1: running
+        dist.barrier()  # 2: leader raised and saw the quiesce
+        st = gate.read()
+        out.update(closed=st.closed, live=st.live_ctas, done=st.tiles_done, claimed=st.tiles_claimed,
+                   seen=st.t_first_seen_ns > 0)
+        dist.barrier()  # 3: state read
+        dist.barrier()  # 4: leader released
+        deadline = time.time() + 30
+        while gate.read().closed and time.time() < deadline:
+            time.sleep(0.001)
+        gate.launch_offline(pool, None, None, 0, 0, None, ctas=8, stream=s.cuda_stream)
+        s.synchronize()
+        st = gate.read()
+        cpp = -(-917504 // 16384)
+        out.update(total=64 * 16 * cpp, final_done=st.tiles_done, final_claimed=st.tiles_claimed)
+    else:  # leader
+        dist.barrier()  # 1
+        time.sleep(0.002)
+        gs = torch.cuda.ExternalStream(gate.stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(gs)
+        group.raise_(1)
+        group.wait_quiesced(1)
+        e1.record(gs)
+        e1.synchronize()
+        out["quiesce_us"] = e0.elapsed_time(e1) * 1e3
+        dist.barrier()  # 2
+        dist.barrier()  # 3: the member has read its gate state
+        group.release(1)
+        torch.cuda.synchronize()
+        dist.barrier()  # 4
+    q.put(out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_tp_group_of_two_processes_shares_the_gate():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {d["rank"]: d for d in (q.get(timeout=300) for _ in range(2))}
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    m = res[1]
+    assert m["closed"] == 1 and m["live"] == 0 and m["seen"]  # the leader's store reached the member
+    assert m["done"] < m["total"]  # preempted mid-pass
+    assert m["done"] == min(m["claimed"], m["total"])  # claimed tiles all finished (context save)
+    assert m["final_done"] == m["total"]  # resumed to completion, each tile once
+    assert res[0]["quiesce_us"] < 1000

@@ -1069,8 +1069,14 @@ struct valve_gate {
   int64_t* d_prefix = nullptr;
   int64_t cap_prefix = 0;
   bool remote = false;  // words opened from another process (CUDA IPC): no stream, no kernels
+  // leader of a TP group: one high-priority helper stream + event per member, so the waits
+  // on the members' acks run concurrently (front-end waits are serial within a stream)
+  std::vector<cudaStream_t> wait_streams;
+  std::vector<cudaEvent_t> wait_events;
   ~valve_gate() {
     if (stream) cudaStreamSynchronize(stream);
+    for (cudaStream_t s : wait_streams) cudaStreamDestroy(s);
+    for (cudaEvent_t e : wait_events) cudaEventDestroy(e);
     if (d && remote) cudaIpcCloseMemHandle(d);
     else if (d) cudaFree(d);
     if (d_prefix) cudaFree(d_prefix);
@@ -1157,13 +1163,20 @@ int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* s) {
     const MemOps& op = memops();
     cudaStream_t st = as_stream(s, g->stream);
     ck(cudaSetDevice(g->device), "cudaSetDevice");
-    std::vector<valve_gate*> all{g};
-    all.insert(all.end(), g->peers.begin(), g->peers.end());
-    for (valve_gate* x : all) {
-      cu_ck(op.wait32((CUstream)st, dptr(&x->d->live_ctas), 0, CU_STREAM_WAIT_VALUE_EQ),
+    // members first, each on its own helper stream (concurrent), joined into `st` by events
+    for (size_t i = 0; i < g->peers.size(); ++i) {
+      cudaStream_t ws = g->wait_streams[i];
+      ck(cudaEventRecord(g->wait_events[2 * i], st), "event");  // order after the raise on st
+      ck(cudaStreamWaitEvent(ws, g->wait_events[2 * i], 0), "event wait");
+      cu_ck(op.wait32((CUstream)ws, dptr(&g->peers[i]->d->live_ctas), 0, CU_STREAM_WAIT_VALUE_EQ),
             "cuStreamWaitValue32");
-      cu_ck(op.write32((CUstream)st, dptr(&x->d->quiesced_gen), gen, 0), "cuStreamWriteValue32");
+      cu_ck(op.write32((CUstream)ws, dptr(&g->peers[i]->d->quiesced_gen), gen, 0), "cuStreamWriteValue32");
+      ck(cudaEventRecord(g->wait_events[2 * i + 1], ws), "event");
     }
+    cu_ck(op.wait32((CUstream)st, dptr(&g->d->live_ctas), 0, CU_STREAM_WAIT_VALUE_EQ), "cuStreamWaitValue32");
+    cu_ck(op.write32((CUstream)st, dptr(&g->d->quiesced_gen), gen, 0), "cuStreamWriteValue32");
+    for (size_t i = 0; i < g->peers.size(); ++i)
+      ck(cudaStreamWaitEvent(st, g->wait_events[2 * i + 1], 0), "event wait");
   });
 }
 
@@ -1217,6 +1230,16 @@ int valve_gate_attach_peers(valve_gate* leader, valve_gate** members, int n) {
         cudaGetLastError();
       }
       leader->peers.push_back(m);
+      int lo = 0, hi = 0;
+      ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+      cudaStream_t ws = nullptr;
+      ck(cudaStreamCreateWithPriority(&ws, cudaStreamNonBlocking, hi), "stream");
+      leader->wait_streams.push_back(ws);
+      for (int e = 0; e < 2; ++e) {
+        cudaEvent_t ev = nullptr;
+        ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        leader->wait_events.push_back(ev);
+      }
     }
   });
 }

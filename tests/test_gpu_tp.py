@@ -94,4 +94,6 @@ def test_tp_group_of_two_processes_shares_the_gate():
     assert m["done"] < m["total"]  # preempted mid-pass
     assert m["done"] == min(m["claimed"], m["total"])  # claimed tiles all finished (context save)
     assert m["final_done"] == m["total"]  # resumed to completion, each tile once
-    assert res[0]["quiesce_us"] < 1000
+    # two processes on one GPU are time-sliced contexts (no MPS): latency here is not the TP
+    # fan-out's (tools/tp_fanout.py measures it); only bound it loosely
+    assert res[0]["quiesce_us"] < 50_000

@@ -139,6 +139,19 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- device arm
 
+def aggregate_ranks(dist, elapsed_ms, total_bytes, device):
+    """Whole-job numbers: the slowest rank's device time and the bytes of all ranks (replicas,
+    weak scaling).  Works on any backend (nccl on GPUs, gloo in the CPU tests)."""
+    import torch
+
+    tt = torch.tensor([elapsed_ms, float(total_bytes)], device=device, dtype=torch.float64)
+    mx = tt.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = tt.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return mx[0].item(), sm[1].item()
+
+
 def link_peak_d2h(torch, dev):
     n = 256 << 20
     d = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -262,12 +275,7 @@ def run_valve(args, rank, world, dist):
     launches = A.kernel_launches() - launches0
     elapsed_ms = t0.elapsed_time(t1)
     if dist:
-        tt = torch.tensor([elapsed_ms, float(total_bytes)], device=dev, dtype=torch.float64)
-        mx = tt.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = tt.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        elapsed_ms, total_bytes = mx[0].item(), sm[1].item()
+        elapsed_ms, total_bytes = aggregate_ranks(dist, elapsed_ms, total_bytes, dev)
 
     # ------------------------------------------------ p50/p99 preempt-to-quiesce
     q = []
@@ -371,7 +379,9 @@ def run_valve(args, rank, world, dist):
     # (real-time loop: random-init Llama-3-8B online in PyTorch + the gated offline tenant on a
     # 32 GiB pool; the 128 GiB reclaim pool is released first)
     rt = {"note": "skipped (--skip-realtime)"}
-    if not args.skip_realtime and not args.profile_mode:
+    if world > 1:
+        rt = {"note": "measured in the N=1 run (one online tenant per node instance)"}
+    elif not args.skip_realtime and not args.profile_mode:
         import gc
 
         del pool, host, gate

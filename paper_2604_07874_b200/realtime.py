@@ -183,6 +183,10 @@ class RunResult:
     quiesce_wait_us: List[float] = field(default_factory=list)
     decode_iter_us: List[float] = field(default_factory=list)
     prefill_us: List[float] = field(default_factory=list)
+    # time the colocation mechanism itself put on each request's critical path: the busy-edge
+    # quiesce wait (CUDA events on the online stream) + page acquisition incl. reclaim (host)
+    mech_ttft_us: Dict[int, float] = field(default_factory=dict)
+    mech_tpot_us: Dict[int, float] = field(default_factory=dict)
 
 
 class Colocation:
@@ -315,6 +319,8 @@ class Colocation:
         lens: Dict[int, int] = {}
         nxt = 0
         busy = False
+        pending_wait = None
+        wait_events = []
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         now_us = lambda: int((time.perf_counter() - t0) * 1e6)  # noqa: E731
@@ -346,13 +352,22 @@ class Colocation:
                 if self.colocated:
                     self.channel.note_busy(now)
                     self._fire_timers(now)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(self.online_stream)
                     self.gate.wait_quiesced(self.channel.disables_issued(), self.online_stream.cuda_stream)
+                    e1.record(self.online_stream)
+                    pending_wait = (e0, e1)  # charged to the request this edge admits
                     self.res.disables = self.channel.disables_issued()
             if queue:  # prefill the queue head
                 r = queue.pop(0)
                 need = -(-r.prompt // self.page_tokens)
                 if self.colocated:
+                    ta = time.perf_counter()
                     self._acquire_online_pages(need, now)
+                    self.res.mech_ttft_us[r.rid] = (time.perf_counter() - ta) * 1e6
+                    if pending_wait is not None:
+                        wait_events.append((r.rid, pending_wait))
+                        pending_wait = None
                 r.pages = need
                 caches[r.rid] = m.alloc()
                 toks = torch.randint(0, m.s.vocab, (r.prompt,), device=m.device)
@@ -369,7 +384,11 @@ class Colocation:
                 tok_after = r.prompt + len(r.emits) + 1
                 need_by.append(max(0, -(-tok_after // self.page_tokens) - r.pages))
             if self.colocated and sum(need_by):
+                ta = time.perf_counter()
                 self._acquire_online_pages(sum(need_by), now)
+                dt = (time.perf_counter() - ta) * 1e6
+                for r in decoding:  # the whole batch waits for the charge
+                    self.res.mech_tpot_us[r.rid] = self.res.mech_tpot_us.get(r.rid, 0.0) + dt
             for r, nb in zip(decoding, need_by):
                 r.pages += nb
             toks = torch.randint(0, m.s.vocab, (len(decoding),), device=m.device)
@@ -396,6 +415,9 @@ class Colocation:
                 self.res.ttft_us[r.rid] = r.first_us - r.arrival_us
         torch.cuda.synchronize()
         self.res.wall_s = time.perf_counter() - t0
+        for rid, (e0, e1) in wait_events:
+            self.res.quiesce_wait_us.append(e0.elapsed_time(e1) * 1e3)
+            self.res.mech_ttft_us[rid] = self.res.mech_ttft_us.get(rid, 0.0) + self.res.quiesce_wait_us[-1]
         if self.colocated:
             gen = self.channel.disables_issued() + 1000
             self.gate.raise_(gen)
@@ -482,6 +504,14 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         "ttft_delta_pct": ttft["mean_pct"], "ttft_delta_max_pct": ttft["max_pct"],
         "tpot_delta_pct": tpot["mean_pct"], "tpot_delta_max_pct": tpot["max_pct"], "pairs": ttft["pairs"],
         "aa_noise_ttft_pct": aa_ttft["mean_pct"], "aa_noise_tpot_pct": aa_tpot["mean_pct"],
+        # the reference DES's view of the same quantity: only the delays the mechanism puts on
+        # the critical path (preempt wait + page acquisition/reclaim), per request, over the
+        # standalone latency -- free of the run-to-run jitter of the end-to-end statistic
+        "ttft_attributable_pct": _attributable(colo.mech_ttft_us, base_ttft, 1),
+        "tpot_attributable_pct": _attributable(colo.mech_tpot_us, base_tpot,
+                                               {r.rid: max(1, r.output - 1) for r in trace}),
+        "preempt_wait_us": {"p50": _median(colo.quiesce_wait_us),
+                            "max": max(colo.quiesce_wait_us) if colo.quiesce_wait_us else None},
         "ttft_ms": {"standalone": mean(base_ttft) / 1e3, "colocated": mean(colo.ttft_us) / 1e3},
         "tpot_ms": {"standalone": mean(base_tpot) / 1e3, "colocated": mean(colo.tpot_us) / 1e3},
         "disables": colo.disables, "disables_per_request": colo.disables / max(1, len(trace)),
@@ -501,6 +531,17 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     return out
+
+
+def _attributable(mech, base, per):
+    """Mean over requests of mechanism delay / standalone latency, in %."""
+    pcts = []
+    for rid, b in base.items():
+        if b <= 0:
+            continue
+        d = mech.get(rid, 0.0) / (per[rid] if isinstance(per, dict) else per)
+        pcts.append(d / b * 100.0)
+    return sum(pcts) / len(pcts) if pcts else None
 
 
 def _median(xs):

@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(kNT)
     k_offline_reserve(PoolDev P, int64_t req, int pages, int64_t t, int max_off) {
   __shared__ int s_row, s_nt, s_fail;
   op_begin(P);
+  if (P.hdr->tombstones > P.HC / 4) ht_rebuild(P, P.s_evrows);  // uniform branch
   if (threadIdx.x == 0) {
     s_row = ht_find(P, req);
     s_nt = 0;

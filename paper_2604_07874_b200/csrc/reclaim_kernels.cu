@@ -25,6 +25,7 @@ static_assert(kSmemHandles * 17 + kSmemListings * 28 + 64 <= 160 * 1024, "greedy
 static_assert(kSmemTuples * 12 <= 160 * 1024, "sort smem");
 
 __device__ long long g_greedy_cycles[2];  // diagnostics: argmin / update cycles of the last run
+__device__ long long g_apply_ns[6];       // diagnostics: apply_core phase stamps of the last run
 
 // Ref lists of instance handle i: CSR (off) or fixed stride with counts (cnt).
 struct Refs {
@@ -388,6 +389,34 @@ __device__ void oracle_core(int n, const int* sorted_ids, int m, const unsigned*
 
 // --------------------------------------------------------------------- apply core
 
+// Warp-wide ascending sort of n (key, payload) pairs in place, any n: the one-direction
+// bitonic network (mirror compare in the first step of each merge, then half-cleaners), with
+// the missing tail treated as +inf -- a pair whose upper index is >= n never swaps.
+__device__ __forceinline__ void warp_sort_asc(uint64_t* key, int* pay, int n, int lane) {
+  int N = 1;
+  while (N < n) N <<= 1;
+  for (int size = 2; size <= N; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < (N >> 1); i += 32) {
+        const int blk = i / stride, off = i % stride;
+        int lo = blk * 2 * stride + off, hi = lo + stride;
+        if (stride == (size >> 1)) hi = (lo | (size - 1)) - off;  // mirror partner
+        if (hi < n) {
+          const uint64_t a = key[lo], b = key[hi];
+          if (a > b) {
+            key[lo] = b;
+            key[hi] = a;
+            const int t = pay[lo];
+            pay[lo] = pay[hi];
+            pay[hi] = t;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 // apply_reclaim (memory.cpp:155-180) for ids[0..k).  Converts the valid prefix (the
 // reference mutates handle by handle and throws at the first bad one), reports the
 // invalidated pages sorted per request, and -- if the whole list was valid -- releases the
@@ -442,6 +471,7 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
   }
   __syncthreads();
   const int nt = s_nt;
+  if (threadIdx.x == 0) g_apply_ns[0] = (long long)globaltimer_ns();
   // evicted rows, then their rank by request id
   int carry = 0;
   for (int base = 0; base < P.R; base += blockDim.x) {
@@ -466,53 +496,88 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
     P.res_evicted[rank] = req;
   }
   __syncthreads();
-  // sort key (request rank, logical page, physical page), payload = block index
-  const bool in_smem = nt <= kSmemTuples;
-  int npow = 1;
-  while (npow < nt) npow <<= 1;
+  if (threadIdx.x == 0) g_apply_ns[1] = (long long)globaltimer_ns();
+  // Report order (request ascending, then logical page, then physical page): a counting sort
+  // by request rank straight into the CSR offsets, then each request's bucket is sorted by
+  // one warp (no CTA barriers).  Key = page << 24 | phys, payload = block index.
+  const bool in_smem = nt <= kSmemTuples && ne <= kSmemTuples;
   uint64_t* key = in_smem ? reinterpret_cast<uint64_t*>(smem) : P.s_key;
-  int* pay = in_smem ? reinterpret_cast<int*>(key + npow) : P.s_pay;
-  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
-    key[i] = ((uint64_t)P.s_rank[P.s_qh[i]] << 48) | ((uint64_t)(uint32_t)P.s_rref[i] << 24) |
-             (uint64_t)(uint32_t)P.s_tphys[i];
-    pay[i] = P.s_tblk[i];
-  }
+  int* pay = in_smem ? reinterpret_cast<int*>(key + kSmemTuples) : P.s_pay;
+  int* bcnt = in_smem ? pay + kSmemTuples : P.s_qcnt;  // [ne] per-request cursor
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) bcnt[e] = 0;
   __syncthreads();
-  block_bitonic_sort(key, pay, nt);
-  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
-    const uint64_t kv = key[i];
-    const int rank = (int)(kv >> 48);
-    P.res_pages[i] = (int64_t)((kv >> 24) & 0xffffffull);
-    P.res_phys[i] = (int)(kv & 0xffffffull);
-    P.res_blk[i] = pay[i];
-    if (i == 0 || (int)(key[i - 1] >> 48) != rank) P.res_inv_off[rank] = i;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) atomicAdd(&bcnt[P.s_rank[P.s_qh[i]]], 1);
+  __syncthreads();
+  carry = 0;
+  for (int base = 0; base < ne; base += blockDim.x) {
+    const int e = base + threadIdx.x;
+    const int c = e < ne ? bcnt[e] : 0;
+    int tot;
+    const int ex = block_excl_scan(c, tot);
+    if (e < ne) P.res_inv_off[e] = carry + ex;
+    carry += tot;
   }
   if (threadIdx.x == 0) P.res_inv_off[ne] = nt;
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) bcnt[e] = 0;
   __syncthreads();
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    const int rank = P.s_rank[P.s_qh[i]];
+    const int pos = P.res_inv_off[rank] + atomicAdd(&bcnt[rank], 1);
+    key[pos] = ((uint64_t)(uint32_t)P.s_rref[i] << 24) | (uint64_t)(uint32_t)P.s_tphys[i];
+    pay[pos] = P.s_tblk[i];
+  }
+  __syncthreads();
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int e = wid; e < ne; e += nw) {
+      const int o = P.res_inv_off[e], n = P.res_inv_off[e + 1] - o;
+      warp_sort_asc(key + o, pay + o, n, lane);
+      for (int i = lane; i < n; i += 32) {
+        const uint64_t kv = key[o + i];
+        P.res_pages[o + i] = (int64_t)(kv >> 24);
+        P.res_phys[o + i] = (int)(kv & 0xffffffull);
+        P.res_blk[o + i] = pay[o + i];
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) g_apply_ns[2] = (long long)globaltimer_ns();
   if (b == k) {
     // Residual pages of evicted requests are plain frees (memory.cpp:176), flattened over
     // (row, block) so the dependent loads of all rows overlap.
+    // (row, block-offset) tables in shared memory when they fit (the sort buffers are free now)
+    const bool sm_rows = ne + 1 <= kSmemTuples;
+    int* qoff = sm_rows ? reinterpret_cast<int*>(smem) : P.s_qoff;
+    int* rows = sm_rows ? qoff + kSmemTuples : P.s_evrows;
+    const bool sm_dec = sm_rows && P.H <= kSmemTuples;
+    int* hdec = rows + kSmemTuples;  // [H] per-handle decrements (sm_dec only)
+    if (sm_dec)
+      for (int h = threadIdx.x; h < P.H; h += blockDim.x) hdec[h] = 0;
     carry = 0;
     for (int base = 0; base < ne; base += blockDim.x) {
       const int e = base + threadIdx.x;
-      const int c = e < ne ? P.row_nblk[P.s_evrows[e]] : 0;
+      const int row = e < ne ? P.s_evrows[e] : 0;
+      const int c = e < ne ? P.row_nblk[row] : 0;
       int tot;
       const int ex = block_excl_scan(c, tot);
-      if (e < ne) P.s_qoff[e] = carry + ex;
+      if (e < ne) {
+        qoff[e] = carry + ex;
+        rows[e] = row;
+      }
       carry += tot;
     }
-    if (threadIdx.x == 0) P.s_qoff[ne] = carry;
+    if (threadIdx.x == 0) qoff[ne] = carry;
     __syncthreads();
     const int total = carry;
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
       int lo = 0, hi = ne - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (P.s_qoff[mid] <= idx) lo = mid;
+        if (qoff[mid] <= idx) lo = mid;
         else hi = mid - 1;
       }
-      const int row = P.s_evrows[lo];
-      const int64_t bi = (int64_t)row * P.P + (idx - P.s_qoff[lo]);
+      const int row = rows[lo];
+      const int64_t bi = (int64_t)row * P.P + (idx - qoff[lo]);
       const int p = P.bt[bi];
       if (p < 0 || p >= P.quarantine) continue;
       P.bt[bi] = P.quarantine;
@@ -521,14 +586,29 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
       P.slot_lid[p] = -1;
       P.slot_blk[p] = -1;
       const int h = p / P.S;
-      if (atomicSub(&P.hused[h], 1) == 1) {
+      if (sm_dec) atomicAdd(&hdec[h], 1);  // aggregated per handle on chip
+      else if (atomicSub(&P.hused[h], 1) == 1) {
         P.hstate[h] = kFree;
         atomicAdd(&s_freed, 1);
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0)
-      for (int e = 0; e < ne; ++e) ht_erase(P, P.row_req[P.s_evrows[e]]);
+    if (sm_dec) {  // one thread per handle applies its decrement; emptied handles go free
+      for (int h = threadIdx.x; h < P.H; h += blockDim.x) {
+        const int d = hdec[h];
+        if (!d) continue;
+        const int left = P.hused[h] - d;
+        P.hused[h] = left;
+        if (left == 0) {
+          P.hstate[h] = kFree;
+          atomicAdd(&s_freed, 1);
+        }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) g_apply_ns[3] = (long long)globaltimer_ns();
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) ht_erase(P, P.row_req[P.s_evrows[e]]);
+    if (threadIdx.x == 0) g_apply_ns[4] = (long long)globaltimer_ns();
   }
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -55,6 +55,7 @@ struct PoolHdr {
   int n_free, n_online, n_offline;
   int ring_head, ring_tail;
   int live_rows;
+  int tombstones;
 };
 
 // Small per-op result block in pinned host memory, written by the op's kernel.
@@ -270,13 +271,18 @@ __device__ __forceinline__ int ht_slot(int64_t key, int HC) {
   return (int)(splitmix64((uint64_t)key) & (uint64_t)(HC - 1));
 }
 
-// Single-thread lookup; returns the row or -1.
+// Request table: linear probing over HC = 2R slots; ht_row = row, -1 empty, -2 tombstone.
+// Deletes leave tombstones so that the erasures of a reclaim can run in parallel (one thread
+// per evicted request); ht_rebuild() compacts the table when tombstones pile up.
+constexpr int kEmpty = -1, kTomb = -2;
+
+// Lookup (any thread); returns the row or -1.
 __device__ __forceinline__ int ht_find(const PoolDev& P, int64_t key) {
   const int mask = P.HC - 1;
   for (int i = ht_slot(key, P.HC), probes = 0; probes < P.HC; i = (i + 1) & mask, ++probes) {
     const int r = P.ht_row[i];
-    if (r < 0) return -1;
-    if (P.ht_key[i] == key) return r;
+    if (r == kEmpty) return -1;
+    if (r >= 0 && P.ht_key[i] == key) return r;
   }
   return -1;
 }
@@ -291,6 +297,7 @@ __device__ __forceinline__ int ht_insert(const PoolDev& P, int64_t key) {
   const int mask = P.HC - 1;
   int i = ht_slot(key, P.HC);
   while (P.ht_row[i] >= 0) i = (i + 1) & mask;
+  if (P.ht_row[i] == kTomb) h->tombstones--;
   P.ht_key[i] = key;
   P.ht_row[i] = row;
   P.row_req[row] = key;
@@ -300,35 +307,49 @@ __device__ __forceinline__ int ht_insert(const PoolDev& P, int64_t key) {
   return row;
 }
 
-// Single-thread delete with backward shift (no tombstones); pushes the row to the ring.
+// Delete (safe for distinct keys in parallel): tombstone the slot, push the row to the ring.
 __device__ __forceinline__ void ht_erase(const PoolDev& P, int64_t key) {
   const int mask = P.HC - 1;
   int i = ht_slot(key, P.HC);
-  while (true) {
-    if (P.ht_row[i] < 0) return;
-    if (P.ht_key[i] == key) break;
-    i = (i + 1) & mask;
+  for (int probes = 0;; i = (i + 1) & mask, ++probes) {
+    const int r = P.ht_row[i];
+    if (r == kEmpty || probes >= P.HC) return;
+    if (r >= 0 && P.ht_key[i] == key) break;
   }
   const int row = P.ht_row[i];
-  P.ht_row[i] = -1;
-  int j = i;
-  while (true) {
-    j = (j + 1) & mask;
-    if (P.ht_row[j] < 0) break;
-    const int k = ht_slot(P.ht_key[j], P.HC);
-    const bool stays = (i <= j) ? (i < k && k <= j) : (i < k || k <= j);
-    if (stays) continue;
-    P.ht_key[i] = P.ht_key[j];
-    P.ht_row[i] = P.ht_row[j];
-    P.ht_row[j] = -1;
-    i = j;
-  }
+  P.ht_row[i] = kTomb;
   PoolHdr* h = P.hdr;
-  P.ring[h->ring_tail % P.R] = row;
-  h->ring_tail++;
-  h->live_rows--;
+  atomicAdd(&h->tombstones, 1);
+  P.ring[atomicAdd(&h->ring_tail, 1) % P.R] = row;
+  atomicSub(&h->live_rows, 1);
   P.row_npages[row] = 0;
   P.row_nblk[row] = 0;
+}
+
+// CTA-wide compaction: gather the live rows, clear, re-insert (CAS probing).  `scratch`
+// holds >= R ints.  Every thread calls.
+__device__ __forceinline__ void ht_rebuild(const PoolDev& P, int* scratch) {
+  __shared__ int s_n;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < P.HC; i += blockDim.x) {
+    const int r = P.ht_row[i];
+    if (r >= 0) scratch[atomicAdd(&s_n, 1)] = r;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < P.HC; i += blockDim.x) P.ht_row[i] = kEmpty;
+  __syncthreads();
+  const int mask = P.HC - 1;
+  for (int j = threadIdx.x; j < s_n; j += blockDim.x) {
+    const int row = scratch[j];
+    const int64_t key = P.row_req[row];
+    int i = ht_slot(key, P.HC);
+    while (atomicCAS(&P.ht_row[i], kEmpty, row) != kEmpty) i = (i + 1) & mask;
+    P.ht_key[i] = key;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) P.hdr->tombstones = 0;
+  __syncthreads();
 }
 
 }  // namespace valve

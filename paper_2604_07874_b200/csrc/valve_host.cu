@@ -608,7 +608,7 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
   });
 }
 
-int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[5]) {
+int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[9]) {
   const int64_t* r = p->mirror->r;
   out[0] = r[4] - r[3];
   out[1] = r[5] - r[4];
@@ -617,6 +617,12 @@ int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[5]) {
   cudaMemcpyFromSymbol(cyc, valve::g_greedy_cycles, sizeof cyc);
   out[3] = cyc[0];
   out[4] = cyc[1];
+  long long an[6] = {0, 0, 0, 0, 0, 0};
+  cudaMemcpyFromSymbol(an, valve::g_apply_ns, sizeof an);
+  out[5] = an[1] - an[0];  // evicted-row compaction + ranks
+  out[6] = an[2] - an[1];  // report sort + outputs
+  out[7] = an[3] - an[2];  // residual page release
+  out[8] = an[4] - an[3];  // request-table erase
   return VALVE_OK;
 }
 

@@ -146,6 +146,12 @@ int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
 int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_bytes,
                                   const valve_copy_params* params);
 int valve_pool_reclaim_copy_wait(valve_pool* p, valve_copy_stats* stats);
+/* Restore (scatter) of host-resident pages into a live request's slots: host page i (of
+ * n_pages, page_bytes each, pinned/mapped) is written to block blk_of_page[i] of `req` -- the
+ * inverse of the gather, e.g. offline weight pages evicted to host by a reclaim (C3) and
+ * re-admitted later.  Synchronous; CTA count / chunk size from params (may be NULL). */
+int valve_pool_restore(valve_pool* p, int64_t req, const void* host_src, int n_pages,
+                       const int* blk_of_page, const valve_copy_params* params, valve_copy_stats* stats);
 /* Pinned, device-mapped host staging for reclaimed pages (cudaHostAlloc, mapped). */
 int valve_host_alloc(int64_t bytes, void** out);
 void valve_host_free(void* p);

@@ -661,6 +661,7 @@ def _declare_valve_extras(L):
         "valve_pool_reclaim_copy_start": (C.c_int, [vp, vp, i64, P(CopyParams)]),
         "valve_pool_reclaim_copy_wait": (C.c_int, [vp, P(CopyStats)]),
         "valve_pool_reclaim_phases": (C.c_int, [vp, P(i64)]),
+        "valve_pool_restore": (C.c_int, [vp, i64, vp, C.c_int, P(C.c_int), P(CopyParams), P(CopyStats)]),
         "valve_host_alloc": (C.c_int, [i64, P(vp)]),
         "valve_host_free": (None, [vp]),
         "valve_pool_fill_pages": (C.c_int, [vp]),
@@ -754,6 +755,20 @@ class DevicePool(MemoryPool):
     def reclaim_copy_wait(self) -> CopyStats:
         st = CopyStats()
         self._b.check(self._b.lib.valve_pool_reclaim_copy_wait(self._h, C.byref(st)))
+        return st
+
+    def restore(self, req: int, host_ptr: int, blocks: Sequence[int],
+                params: Optional[CopyParams] = None) -> CopyStats:
+        """Scatter host pages back into `req`'s slots: host page i -> block blocks[i]
+        (the inverse of reclaim_copy for a request re-reserved after eviction)."""
+        n = len(blocks)
+        b = _arr(C.c_int, n)
+        for i, x in enumerate(blocks):
+            b[i] = int(x)
+        st = CopyStats()
+        self._b.check(self._b.lib.valve_pool_restore(
+            self._h, int(req), C.c_void_p(host_ptr), n, _ptr(b, C.c_int),
+            C.byref(params) if params is not None else None, C.byref(st)))
         return st
 
     def reclaim_phases_us(self):

@@ -177,4 +177,46 @@ __global__ void __launch_bounds__(32) k_reclaim_copy_tma(CopyArgs A) {
   atomicMax(A.t_last, globaltimer_ns());
 }
 
+// Scatter of host-resident pages back into HBM (the restore side of a reclaim that copied,
+// e.g. evicted offline weight pages): host page i goes to block blk_of_page[i] of the
+// request, i.e. to physical slot bt_row[blk]; 16-byte loads from the host-mapped source
+// (PCIe reads), 16-byte stores to HBM.  Chunks are claimed from an HBM cursor.
+__global__ void __launch_bounds__(512) k_restore_scatter(ScatterArgs A) {
+  __shared__ long long s_chunk;
+  const int64_t cpp = (A.page_bytes + A.chunk_bytes - 1) / A.chunk_bytes;
+  for (;;) {
+    if (threadIdx.x == 0) s_chunk = (long long)atomicAdd(A.cursor, 1ull);
+    __syncthreads();
+    const long long c = s_chunk;
+    __syncthreads();
+    if (c >= A.n_chunks) break;
+    const int64_t page = c / cpp;
+    const int64_t off = (c % cpp) * A.chunk_bytes;
+    const int64_t len = min(A.chunk_bytes, A.page_bytes - off);
+    const int blk = A.blk_of_page[page];
+    const int phys = blk < *A.nblk ? A.bt_row[blk] : -1;
+    if (phys < 0 || phys >= A.quarantine) {
+      if (threadIdx.x == 0 && off == 0) atomicAdd(A.bad, 1ull);
+      continue;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(A.src + page * A.page_bytes + off);
+    uint4* dst = reinterpret_cast<uint4*>(A.pages + (int64_t)phys * A.slot_bytes + off);
+    const int nvec = (int)(len >> 4);
+    const int step = blockDim.x * kVec;
+    for (int base = 0; base < nvec; base += step) {
+      uint4 v[kVec];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) {
+        const int i = base + u * blockDim.x + threadIdx.x;
+        if (i < nvec) v[u] = src[i];
+      }
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) {
+        const int i = base + u * blockDim.x + threadIdx.x;
+        if (i < nvec) dst[i] = v[u];
+      }
+    }
+  }
+}
+
 }  // namespace valve

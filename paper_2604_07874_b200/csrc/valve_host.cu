@@ -284,7 +284,7 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   d.res_phys = p->dalloc<int>(HS);
   d.res_blk = p->dalloc<int>(HS);
   d.res_counts = p->dalloc<int>(4);
-  p->d_ids = p->dalloc<int>(std::max(H, 1) * 2);
+  p->d_ids = p->dalloc<int>(std::max(std::max(H, 1) * 2, p->Pblk));
   p->d_in64 = p->dalloc<int64_t>(R);
   p->d_in64b = p->dalloc<int64_t>(R);
   p->d_copyctr = p->dalloc<unsigned long long>(4);
@@ -753,6 +753,72 @@ int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
   const int rc = valve_pool_reclaim_copy_start(p, host_dst, dst_bytes, prm);
   if (rc != VALVE_OK) return rc;
   return valve_pool_reclaim_copy_wait(p, st);
+}
+
+int valve_pool_restore(valve_pool* p, int64_t req, const void* host_src, int n_pages,
+                       const int* blk_of_page, const valve_copy_params* prm, valve_copy_stats* st) {
+  return guard([&] {
+    valve_copy_params c;
+    valve_copy_params_default(&c);
+    if (prm) c = *prm;
+    if (c.ctas <= 0) c.ctas = 16;
+    if (c.threads <= 0 || c.threads > 512 || c.threads % 32) c.threads = 512;
+    if (c.chunk_bytes <= 0 || c.chunk_bytes % 16) c.chunk_bytes = 65536;
+    if (!p->d.pages) fail(VALVE_LOGIC_ERROR, "restore: pool has no page store");
+    if (n_pages < 0 || n_pages > p->Pblk) fail(VALVE_INVALID_ARGUMENT, "restore: bad page count");
+    if (n_pages && !blk_of_page) fail(VALVE_INVALID_ARGUMENT, "restore: null block list");
+    for (int i = 0; i < n_pages; ++i)
+      if (blk_of_page[i] < 0 || blk_of_page[i] >= p->Pblk)
+        fail(VALVE_OUT_OF_RANGE, "restore: block index out of range");
+    if (reinterpret_cast<uintptr_t>(host_src) % 16)
+      fail(VALVE_INVALID_ARGUMENT, "restore: source must be 16-byte aligned");
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    p->order_after_copy();
+    // the request's row (device lookup) -> block table row pointer
+    k_offline_pages_of<<<1, 32, 0, p->stream>>>(p->d, req);
+    counted();
+    p->sync_and_check("restore");
+    const int row = (int)p->mirror->r[1];
+    if (row < 0) fail(VALVE_LOGIC_ERROR, "restore: request holds no pages (reserve it first)");
+    if (n_pages == 0) return;
+    const void* dsrc = nullptr;
+    ck(cudaHostGetDevicePointer(const_cast<void**>(&dsrc), const_cast<void*>(host_src), 0),
+       "restore: source is not pinned/mapped host memory");
+    ck(cudaMemcpyAsync(p->d_ids, blk_of_page, (size_t)n_pages * 4, cudaMemcpyHostToDevice, p->stream),
+       "upload");
+    ScatterArgs A{};
+    A.pages = p->d.pages;
+    A.slot_bytes = p->d.slot_bytes;
+    A.page_bytes = p->d.page_bytes;
+    A.chunk_bytes = c.chunk_bytes;
+    A.bt_row = p->d.bt + (int64_t)row * p->Pblk;
+    A.nblk = p->d.row_nblk + row;
+    A.blk_of_page = p->d_ids;
+    A.n_pages = n_pages;
+    A.n_chunks = (int64_t)n_pages * ((A.page_bytes + c.chunk_bytes - 1) / c.chunk_bytes);
+    A.src = static_cast<const uint8_t*>(dsrc);
+    A.quarantine = p->d.quarantine;
+    ck(cudaMemsetAsync(p->d_copyctr, 0, 32, p->stream), "memset");
+    A.cursor = p->d_copyctr;
+    A.bad = p->d_copyctr + 3;
+    ck(cudaEventRecord(p->ev0, p->stream), "event");
+    k_restore_scatter<<<c.ctas, c.threads, 0, p->stream>>>(A);
+    counted();
+    ck(cudaEventRecord(p->ev1, p->stream), "event");
+    ck(cudaGetLastError(), "restore launch");
+    ck(cudaStreamSynchronize(p->stream), "restore");
+    unsigned long long bad = 0;
+    ck(cudaMemcpy(&bad, p->d_copyctr + 3, 8, cudaMemcpyDeviceToHost), "read");
+    if (bad) fail(VALVE_LOGIC_ERROR, "restore: a block of the request is not mapped");
+    if (st) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, p->ev0, p->ev1), "event");
+      st->bytes = (int64_t)n_pages * p->d.page_bytes;
+      st->pages = n_pages;
+      st->kernel_ms = ms;
+      st->t_first_ns = st->t_last_ns = 0;
+    }
+  });
 }
 
 int valve_host_alloc(int64_t bytes, void** out) {

@@ -62,6 +62,22 @@ struct CopyArgs {
 __global__ void k_reclaim_copy(CopyArgs A);
 __global__ void k_reclaim_copy_tma(CopyArgs A);
 
+// restore scatter (copy_kernels.cu): host pages back into a request's (re-reserved) slots
+struct ScatterArgs {
+  uint8_t* pages;
+  int64_t slot_bytes, page_bytes, chunk_bytes;
+  const int* bt_row;       // the request's block table row
+  const int* blk_of_page;  // block index of host page i
+  const int* nblk;         // the request's mapped block count
+  int n_pages;
+  int64_t n_chunks;
+  const uint8_t* src;      // device alias of pinned host memory (n_pages * page_bytes)
+  int quarantine;
+  unsigned long long* cursor;
+  unsigned long long* bad;  // pages whose block is not mapped (skipped)
+};
+__global__ void k_restore_scatter(ScatterArgs A);
+
 // gate (gate_kernels.cu)
 // The tile space of a work list is split into kStripes contiguous stripes, each with its own
 // claim cursor (a single cursor saturates one L2 atomic unit at ~9k claiming warps).

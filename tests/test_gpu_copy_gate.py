@@ -208,3 +208,76 @@ def test_async_copy_overlaps_bookkeeping(oracle_c):
     assert st.bytes == n_pages * pool.page_bytes
     assert np.array_equal(buf.view(), _expected_images(oracle_c, res, pool.page_bytes))
     pool.check_invariants()
+
+
+# ------------------------------------------------------------------- weight pages (C3)
+
+@pytest.mark.parametrize("slot,page,n_w", [(16384, 12288, 21), (1 << 20, 917504, 48)])
+def test_weight_pages_evict_restore_round_trip(oracle_c, slot, page, n_w):
+    """Offline weight pages evicted with their handles go to host (gather) and come back
+    (scatter) into freshly reserved slots; a second eviction must gather the same bytes."""
+    rng = random.Random(slot + n_w)
+    H, S = 24, 8
+    W = 1_000_003
+    pool = A.DevicePool(H, S, 16, slot_bytes=slot, page_bytes=page)
+    assert pool.offline_reserve(W, n_w, 0)
+    kv = [r for r in range(30) if pool.offline_reserve(r, rng.randint(1, 6), 1)]
+    pool.fill_pages()
+    blocks_w = list(range(n_w))
+    # evict every handle holding a weight page
+    res = pool.apply_reclaim(sorted(pool.handles_of_request(W)), 10)
+    assert W in res.evicted_requests
+    n = sum(len(v) for v in res.invalidated_pages.values())
+    buf = A.HostBuffer(n * page)
+    pool.reclaim_copy(buf.ptr, buf.nbytes, A.copy_params(ctas=4, chunk_bytes=4096))
+    img = buf.view()
+    assert np.array_equal(img, _expected_images(oracle_c, res, page))
+    # weight pages out of the report, in block order, into their own staging buffer
+    off, pos = 0, {}
+    for r in res.evicted_requests:
+        for b in res.block_index[r]:
+            if r == W:
+                pos[b] = off
+            off += 1
+    assert sorted(pos) == blocks_w
+    wbuf = A.HostBuffer(n_w * page)
+    order = rng.sample(blocks_w, n_w)  # restore takes any page -> block order
+    for i, b in enumerate(order):
+        wbuf.view()[i * page:(i + 1) * page] = img[pos[b] * page:(pos[b] + 1) * page]
+    # give the handles back, let other requests churn the freed slots, re-admit the weights
+    pool.online_release(len(res.handles))
+    for r in range(100, 110):
+        pool.offline_reserve(r, rng.randint(1, 4), 20)
+    pool.fill_pages()
+    assert pool.offline_reserve(W, n_w, 30)
+    st = pool.restore(W, wbuf.ptr, order, A.copy_params(ctas=8, chunk_bytes=8192))
+    assert st.bytes == n_w * page and st.kernel_ms > 0
+    # second eviction: the weights' bytes must be the original images again
+    res2 = pool.apply_reclaim(sorted(pool.handles_of_request(W)), 40)
+    n2 = sum(len(v) for v in res2.invalidated_pages.values())
+    buf2 = A.HostBuffer(n2 * page)
+    pool.reclaim_copy(buf2.ptr, buf2.nbytes)
+    got = buf2.view()
+    want = _expected_images(oracle_c, res2, page)
+    off = 0
+    for r in res2.evicted_requests:
+        k = len(res2.block_index[r])
+        sl = slice(off * page, (off + k) * page)
+        if r == W:
+            assert np.array_equal(got[sl], want[sl])
+        off += k
+    assert W in res2.evicted_requests
+
+
+def test_restore_rejects_bad_blocks():
+    pool = A.DevicePool(8, 4, 16, slot_bytes=4096, page_bytes=4096)
+    buf = A.HostBuffer(4 * 4096)
+    with pytest.raises(A.LogicError):
+        pool.restore(5, buf.ptr, [0])  # not reserved
+    assert pool.offline_reserve(5, 3, 0)
+    with pytest.raises(A.OutOfRange):
+        pool.restore(5, buf.ptr, [0, 1 << 20])
+    with pytest.raises(A.LogicError):
+        pool.restore(5, buf.ptr, [3])  # block 3 is not mapped (3 pages)
+    pool.restore(5, buf.ptr, [2, 0, 1])
+    pool.check_invariants()

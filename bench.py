@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=2604)
     ap.add_argument("--skip-realtime", action="store_true", help="skip the measured TTFT/TPOT run")
     ap.add_argument("--rt-horizon", type=float, default=24.0, help="online trace length (s)")
+    ap.add_argument("--rt-repeats", type=int, default=2, help="colocated runs (interleaved with standalone)")
     ap.add_argument("--profile-mode", action="store_true",
                     help="ncu launch-list runs: no offline kernel (ncu serialises it to completion)")
     return ap.parse_args()
@@ -199,9 +200,9 @@ def run_valve(args, rank, world, dist):
     def ev():
         return torch.cuda.Event(enable_timing=True)
 
-    def restore(evicted):
+    def restore(evicted, n_release=None):
         nonlocal next_req, t
-        pool.online_release(args.k)
+        pool.online_release(n_release or args.k)
         costs = {}
         for r in evicted:  # re-admission of the evicted requests (resume recompute)
             pages, cost = live.pop(r)
@@ -325,6 +326,24 @@ def run_valve(args, rank, world, dist):
     ce_gbs = ce.bytes / (ce.kernel_ms * 1e-3) / 1e9
     restore(pool.last_reclaim().evicted_requests)
 
+    # ------------------------------------------------ eviction-policy contrast on the device
+    # (SURVEY §8f.4): Algorithm 1 vs FIFO (the uvm/static baseline, reclaim.cpp:69-83) on the
+    # same C2 snapshots, both selected by the device kernels; cost = recompute tokens evicted
+    # (reclaim.cpp:19-31 evicted_cost, also on the device)
+    contrast = {}
+    for kk in sorted({8, args.k}):
+        sel_c = fifo_c = 0
+        for _ in range(4):
+            inst = pool.snapshot()
+            inst.cost = {r: live[r][1] for h in inst.handles for r in h.requests}
+            sel_c += A.evicted_cost(inst, A.selective_reclaim(inst, kk, device=gpu), device=gpu)
+            fifo_c += A.evicted_cost(inst, A.fifo_reclaim(inst, kk, device=gpu), device=gpu)
+            t += 10
+            nh, _, _ = pool.reclaim(kk, t, 0)  # churn the pool between samples
+            restore(pool.last_reclaim().evicted_requests, nh)
+        contrast[f"k{kk}"] = {"selective_tokens": sel_c, "fifo_tokens": fifo_c,
+                              "reduction_pct": round((1 - sel_c / fifo_c) * 100, 2) if fifo_c else None}
+
     # ------------------------------------------------ e2e through the reference-facing API
     e2e_bytes = e2e_h2d = e2e_d2h = 0
     brk = {"quiesce": 0.0, "snapshot": 0.0, "select": 0.0, "apply": 0.0, "restore": 0.0, "copy_wait": 0.0}
@@ -391,7 +410,8 @@ def run_valve(args, rank, world, dist):
         from paper_2604_07874_b200 import realtime as RT
 
         # offline harvest at one 8-warp CTA per SM (~3.7 TB/s of HBM reads in the gaps)
-        rt = RT.measure_deltas(horizon=args.rt_horizon, device=gpu, seed=args.seed + rank, offline_ctas=148)
+        rt = RT.measure_deltas(horizon=args.rt_horizon, device=gpu, seed=args.seed + rank, offline_ctas=148,
+                               repeats=args.rt_repeats)
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "r1_copy_traffic.json")))
     except OSError:
@@ -436,6 +456,7 @@ def run_valve(args, rank, world, dist):
         "step_quiesce_us_mean": round(statistics.mean(stats["quiesce_us"]), 1),
         "offline_polling_overhead_pct": round((1 - polled[0] / unpolled[0]) * 100, 2),
         "offline_gbs": {"polled": round(polled[0], 1), "unpolled": round(unpolled[0], 1)},
+        "policy_contrast_recompute": contrast,
         "ttft_delta_pct": rt.get("ttft_delta_pct"),
         "tpot_delta_pct": rt.get("tpot_delta_pct"),
         "online_realtime": rt,

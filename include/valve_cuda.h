@@ -263,6 +263,23 @@ int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work*
 /* Resets the tile cursor / statistics (new work). */
 int valve_offline_reset(valve_gate* g);
 
+/* Gated offline GEMM: C = A * B^T in bf16 with fp32 accumulation on the tcgen05
+ * tensor cores (TMA-fed, TMEM accumulator), persistent over 128 x 256 tiles of C claimed from
+ * the gate's tile cursors -- the compute-bound half of an offline decode iteration (the
+ * projection GEMMs), preempted at tile granularity like valve_offline_launch.  All pointers are
+ * device memory; m % 128 == 0, n % 256 == 0, k % 64 == 0, rows 16-byte aligned. */
+typedef struct {
+  const void* a;  /* bf16 [m, k] row-major (activations) */
+  const void* b;  /* bf16 [n, k] row-major (weight, nn.Linear layout) */
+  void* c;        /* bf16 [m, n] row-major */
+  int m, n, k;
+  int ctas;       /* 0 = one CTA per SM */
+  int poll;       /* 0 = ignore the gate (overhead baseline) */
+  int fresh;      /* nonzero: a new work list -- zero the tile cursors and counters on the launch
+                     stream first (stream-ordered valve_offline_reset); 0: resume */
+} valve_offline_gemm_work;
+int valve_offline_gemm(valve_gate* g, const valve_offline_gemm_work* w, void* stream);
+
 /* ============================================================ channel controller (b1, b2) */
 /* channel.hpp:30-80 state machine with C hooks; optionally bound to a device gate so
  * disable/enable raise/release it (valve_channel_bind_gate). */

@@ -639,6 +639,11 @@ class OfflineWork(C.Structure):
                 ("poll", C.c_int), ("tile_bytes", i64)]
 
 
+class OfflineGemmWork(C.Structure):
+    _fields_ = [("a", C.c_void_p), ("b", C.c_void_p), ("c", C.c_void_p), ("m", C.c_int), ("n", C.c_int),
+                ("k", C.c_int), ("ctas", C.c_int), ("poll", C.c_int), ("fresh", C.c_int)]
+
+
 class PoolView(C.Structure):
     _fields_ = [("pages", C.c_void_p), ("block_tables", C.c_void_p), ("slot_bytes", i64),
                 ("page_bytes", i64), ("max_pages_per_request", C.c_int),
@@ -680,6 +685,7 @@ def _declare_valve_extras(L):
         "valve_gate_stream": (vp, [vp]),
         "valve_offline_launch": (C.c_int, [vp, vp, P(OfflineWork), vp]),
         "valve_offline_reset": (C.c_int, [vp]),
+        "valve_offline_gemm": (C.c_int, [vp, P(OfflineGemmWork), vp]),
         "valve_channel_bind_gate": (C.c_int, [vp, vp]),
     }
     for name, (res, args) in sig.items():
@@ -888,6 +894,15 @@ class Gate:
 
     def reset_work(self):
         self._b.check(self._b.lib.valve_offline_reset(self._h))
+
+    def launch_gemm(self, a_ptr: int, b_ptr: int, c_ptr: int, m: int, n: int, k: int, *, ctas: int = 0,
+                    poll: bool = True, stream: Optional[int] = None, fresh: bool = False):
+        """Gated tcgen05 GEMM C[m,n] = A[m,k] B[n,k]^T (bf16, device pointers), preemptible at
+        128x256-tile granularity (valve_offline_gemm).  fresh=True starts a new work list
+        (stream-ordered cursor reset); otherwise the launch resumes from the gate's cursors."""
+        w = OfflineGemmWork(a_ptr, b_ptr, c_ptr, m, n, k, ctas, 1 if poll else 0, 1 if fresh else 0)
+        self._b.check(self._b.lib.valve_offline_gemm(self._h, C.byref(w),
+                                                     C.c_void_p(stream) if stream else None))
 
     def launch_offline(self, pool: DevicePool, rows_ptr: Optional[int], npages_ptr: Optional[int],
                        n_requests: int, total_tiles: int, out_ptr: Optional[int], *, ctas: int = 0,

@@ -1,0 +1,243 @@
+// gemm_kernels.cu -- the gated offline GEMM: a persistent tcgen05/TMA bf16 GEMM whose tile loop
+// honours the preemption gate ("persistent tile-looped kernels, GEMM via tcgen05
+// tiles ... every tile executes exactly once across preemptions").
+//
+// C[m, n] = sum_k A[m, k] * B[n, k]   (A activations, B an nn.Linear weight, both K-major bf16,
+// fp32 accumulation in TMEM, bf16 output).
+//
+// Per CTA (one per SM, 256 threads):
+//   warp 0 lane 0 : TMA producer  -- 128x64 A box + 256x64 B box per k-block, SWIZZLE_128B,
+//                                    into a kStages-deep smem ring (full/empty mbarriers)
+//   warp 1 lane 0 : MMA issuer    -- 4 x tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256,
+//                                    K=16) per k-block, tcgen05.commit frees the smem stage
+//   warp 2        : TMEM owner    -- tcgen05.alloc / dealloc of 256 fp32 columns
+//   warps 4..7    : epilogue      -- tcgen05.ld 32x32b.x32, bf16 pack, 16-byte global stores
+// Tiles (128 x 256 of C) are claimed from the gate's striped HBM cursors by thread 0 after reading the
+// gate word; a closed gate ends the loop, so the in-flight tile always completes (quiesce <= one
+// tile) and unclaimed tiles resume on the next launch.  The CTA's retirement is the same
+// live_ctas ack the decode kernel gives (gate_kernels.cu).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "valve_kernels.h"
+
+namespace valve {
+
+namespace {
+
+constexpr int kBM = 128, kBN = 256, kBK = 64, kUK = 16;
+constexpr int kABytes = kBM * kBK * 2;  // 16 KiB
+constexpr int kBBytes = kBN * kBK * 2;  // 32 KiB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr uint32_t kTmemCols = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+// K-major operand tile written by TMA with SWIZZLE_128B: 128-byte rows, 8-row (1024 B) atoms
+// stacked along M/N -> stride byte offset 1024, layout type 2 (SWIZZLE_128B), descriptor
+// version 1 (sm_100).  Advancing K by 16 bf16 inside the 128-byte atom moves the start by 32 B.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N = 256, M = 128
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                            ((uint32_t)(kBM >> 4) << 24);
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256, 1)
+    k_offline_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   GemmArgs G) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kGemmStages], empty_bar[kGemmStages], tmem_full;
+  __shared__ uint32_t s_tmem;
+  __shared__ long long s_tile;
+  // 1024-byte alignment for the swizzled operand tiles
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGemmStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = s_tmem;
+  const int tiles_n = G.n / kBN;
+  const int kblocks = G.k / kBK;
+  uint32_t it0 = 0;  // k-blocks this CTA has streamed: the smem ring position of both roles
+  uint32_t acc_phase = 0;
+  unsigned long long done = 0;
+  const unsigned long long total = (unsigned long long)G.total_tiles;
+  const unsigned long long per = (total + kStripes - 1) / kStripes;
+  int stripe = blockIdx.x % kStripes, visited = 0;  // thread 0 state (same claim order as decode)
+  for (;;) {
+    if (threadIdx.x == 0) {
+      long long t = -1;
+      if (G.poll && ld_acquire(&G.g->closed)) {
+        atomicCAS(&G.g->t_first_seen, 0ull, globaltimer_ns());
+      } else {
+        while (visited < kStripes) {
+          const unsigned long long local = atomicAdd(&G.g->cursor[stripe], 1ull);
+          const unsigned long long c = (unsigned long long)stripe * per + local;
+          if (local < per && c < total) {
+            t = (long long)c;
+            break;
+          }
+          stripe = (stripe + 1) % kStripes;
+          ++visited;
+        }
+      }
+      s_tile = t;
+    }
+    __syncthreads();
+    const long long tile = s_tile;
+    if (tile < 0) break;
+    const int m0 = (int)(tile / tiles_n) * kBM;
+    const int n0 = (int)(tile % tiles_n) * kBN;
+    if (warp == 0 && lane == 0) {
+      // ---------------- TMA producer
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const uint32_t st = (it0 + kb) % kGemmStages, ph = ((it0 + kb) / kGemmStages) & 1u;
+        mbar_wait(&empty_bar[st], ph ^ 1);
+        uint8_t* sa = smem + st * kStageBytes;
+        uint8_t* sb = sa + kABytes;
+        mbar_expect_tx(&full_bar[st], kStageBytes);
+        tma_load_2d(sa, &map_a, &full_bar[st], kb * kBK, m0);
+        tma_load_2d(sb, &map_b, &full_bar[st], kb * kBK, n0);
+      }
+    } else if (warp == 1 && lane == 0) {
+      // ---------------- MMA issuer
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const uint32_t st = (it0 + kb) % kGemmStages, ph = ((it0 + kb) / kGemmStages) & 1u;
+        mbar_wait(&full_bar[st], ph);
+        fence_after();
+        const uint32_t sa = smem_u32(smem + st * kStageBytes);
+        const uint32_t sb = sa + kABytes;
+#pragma unroll
+        for (int k = 0; k < kBK / kUK; ++k)
+          mma_bf16(tmem, smem_desc(sa + k * kUK * 2), smem_desc(sb + k * kUK * 2), (kb | k) != 0);
+        mma_commit(&empty_bar[st]);  // the stage is free once these MMAs have read it
+      }
+      mma_commit(&tmem_full);  // accumulator complete
+    } else if (warp >= 4) {
+      // ---------------- epilogue: TMEM lanes 32*(warp-4).. -> rows of C
+      mbar_wait(&tmem_full, acc_phase);
+      fence_after();
+      const int q = warp - 4;
+      const int row = m0 + q * 32 + lane;
+      __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(G.c) + (int64_t)row * G.n + n0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < kBN; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint4* dst = reinterpret_cast<uint4*>(crow + c0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(pack_bf16(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
+                              pack_bf16(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                              pack_bf16(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                              pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+      }
+      fence_before();
+    }
+    it0 += (uint32_t)kblocks;
+    acc_phase ^= 1;
+    ++done;
+    __syncthreads();  // TMEM drained before the next tile's first MMA overwrites it
+    fence_after();
+  }
+  if (threadIdx.x == 0) {
+    if (done) atomicAdd(&G.g->tiles_done, done);
+    __threadfence();
+    if (atomicSub(&G.g->live_ctas, 1u) == 1u) {
+      G.g->t_quiesced = globaltimer_ns();
+      __threadfence_system();
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+}  // namespace valve

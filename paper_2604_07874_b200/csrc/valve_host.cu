@@ -1141,12 +1141,17 @@ struct valve_gate {
   int64_t* d_prefix = nullptr;
   int64_t cap_prefix = 0;
   bool remote = false;  // words opened from another process (CUDA IPC): no stream, no kernels
+  cudaStream_t work_stream = nullptr;  // default stream of gated work launched without one
   // leader of a TP group: one high-priority helper stream + event per member, so the waits
   // on the members' acks run concurrently (front-end waits are serial within a stream)
   std::vector<cudaStream_t> wait_streams;
   std::vector<cudaEvent_t> wait_events;
   ~valve_gate() {
     if (stream) cudaStreamSynchronize(stream);
+    if (work_stream) {
+      cudaStreamSynchronize(work_stream);
+      cudaStreamDestroy(work_stream);
+    }
     for (cudaStream_t s : wait_streams) cudaStreamDestroy(s);
     for (cudaEvent_t e : wait_events) cudaEventDestroy(e);
     if (d && remote) cudaIpcCloseMemHandle(d);
@@ -1402,6 +1407,80 @@ int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work*
     k_offline_decode<<<ctas, threads, 0, st>>>(A);
     counted();
     ck(cudaGetLastError(), "offline launch");
+  });
+}
+
+namespace {
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled encode_tiled() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q);
+  });
+  if (!fn) fail(VALVE_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable in this driver");
+  return fn;
+}
+// K-major bf16 [rows, k] -> boxes of box_rows x 64 (128 B, the SWIZZLE_128B span)
+CUtensorMap kmajor_map(const void* base, int rows, int k, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)k * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  cu_ck(encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+        "cuTensorMapEncodeTiled");
+  return m;
+}
+}  // namespace
+
+int valve_offline_gemm(valve_gate* g, const valve_offline_gemm_work* w, void* s) {
+  return guard([&] {
+    const MemOps& op = memops();
+    if (g->remote) fail(VALVE_LOGIC_ERROR, "offline_gemm: remote gate (launch on the owning process)");
+    if (!w || !w->a || !w->b || !w->c) fail(VALVE_INVALID_ARGUMENT, "offline_gemm: null operand");
+    if (w->m <= 0 || w->n <= 0 || w->k <= 0 || w->m % 128 || w->n % 256 || w->k % 64)
+      fail(VALVE_INVALID_ARGUMENT, "offline_gemm: need m % 128 == 0, n % 256 == 0, k % 64 == 0");
+    if ((reinterpret_cast<uintptr_t>(w->a) | reinterpret_cast<uintptr_t>(w->b) |
+         reinterpret_cast<uintptr_t>(w->c)) % 16)
+      fail(VALVE_INVALID_ARGUMENT, "offline_gemm: operands must be 16-byte aligned");
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    // never the gate's own stream: the raise must be able to overtake the running work
+    if (!s && !g->work_stream)
+      ck(cudaStreamCreateWithFlags(&g->work_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cudaStream_t st = as_stream(s, g->work_stream);
+    static std::once_flag attr_once;
+    std::call_once(attr_once, [] {
+      cudaFuncSetAttribute(k_offline_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
+    });
+    const CUtensorMap ma = kmajor_map(w->a, w->m, w->k, 128);
+    const CUtensorMap mb = kmajor_map(w->b, w->n, w->k, 256);
+    int ctas = w->ctas;
+    if (ctas <= 0) ck(cudaDeviceGetAttribute(&ctas, cudaDevAttrMultiProcessorCount, g->device), "attr");
+    GemmArgs G{};
+    G.g = g->d;
+    G.c = w->c;
+    G.m = w->m;
+    G.n = w->n;
+    G.k = w->k;
+    G.total_tiles = (long long)(w->m / 128) * (w->n / 256);
+    G.poll = w->poll;
+    ctas = (int)std::min<long long>(ctas, G.total_tiles);
+    if (w->fresh) {
+      ck(cudaMemsetAsync(&g->d->t_first_seen, 0, 4 * sizeof(unsigned long long), st), "memset");
+      ck(cudaMemsetAsync(g->d->cursor, 0, sizeof(g->d->cursor), st), "memset");
+    }
+    cu_ck(op.write64((CUstream)st, dptr(&g->d->total), (cuuint64_t)G.total_tiles, 0), "cuStreamWriteValue64");
+    cu_ck(op.wait32((CUstream)st, dptr(&g->d->closed), 0, CU_STREAM_WAIT_VALUE_EQ), "cuStreamWaitValue32");
+    cu_ck(op.write32((CUstream)st, dptr(&g->d->live_ctas), (cuuint32_t)ctas, 0), "cuStreamWriteValue32");
+    k_offline_gemm<<<ctas, 256, kGemmSmemBytes, st>>>(ma, mb, G);
+    counted();
+    ck(cudaGetLastError(), "offline gemm launch");
   });
 }
 

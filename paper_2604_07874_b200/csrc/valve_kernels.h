@@ -1,5 +1,7 @@
 // valve_kernels.h -- kernel entry points shared between the .cu translation units.
 #pragma once
+#include <cuda.h>
+
 #include "valve_common.cuh"
 
 namespace valve {
@@ -111,5 +113,18 @@ struct OfflineArgs {
   int poll;
 };
 __global__ void k_offline_decode(OfflineArgs A);
+
+// gated offline GEMM (gemm_kernels.cu): 128x256 tiles claimed from the gate's striped cursors
+constexpr int kGemmStages = 4;
+constexpr int kGemmSmemBytes = kGemmStages * (128 * 64 + 256 * 64) * 2 + 1024;
+struct GemmArgs {
+  GateDev* g;
+  void* c;  // bf16 [m, n]
+  int m, n, k;
+  long long total_tiles;
+  int poll;
+};
+__global__ void k_offline_gemm(const __grid_constant__ CUtensorMap map_a,
+                               const __grid_constant__ CUtensorMap map_b, GemmArgs G);
 
 }  // namespace valve

@@ -463,35 +463,58 @@ def warm_shapes(model: OnlineModel, trace: List[OnlineReq]):
     torch.cuda.synchronize()
 
 
+def _avg_runs(dicts):
+    """Per-request mean over runs (requests present in every run)."""
+    keys = set(dicts[0])
+    for d in dicts[1:]:
+        keys &= set(d)
+    return {k: sum(d[k] for d in dicts) / len(dicts) for k in sorted(keys)}
+
+
 def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, handles=256, seed=2604,
-                   output=(8, 12), prompt=(2500, 3500), layers=32, device=0, offline_ctas=0):
+                   output=(8, 12), prompt=(2500, 3500), layers=32, device=0, offline_ctas=0, repeats=1):
     """Paired standalone vs colocated run of one online trace (default: the pair_06 shape --
     spike base 0.3/s, 6/s for 1 s every 8 s, prompt 2500-3500, output 8-12 -- so the online
     lane goes idle and the offline tenant harvests the gaps).  Returns the reference's paired
-    TTFT/TPOT increases (metrics.cpp:49-65) plus harvest statistics."""
+    TTFT/TPOT increases (metrics.cpp:49-65) plus harvest statistics.
+
+    Runs are interleaved A B A B ... A (`repeats` colocated runs between repeats+1 standalone
+    ones): each request's latency is averaged over its standalone runs and over its colocated
+    runs before pairing, which cancels clock/thermal drift and shrinks the batching-order jitter
+    of a real-time loop by sqrt(repeats).  The A/A noise floor pairs the even standalone runs
+    against the odd ones (the same statistic with no mechanism in it)."""
     dev = torch.device("cuda", device)
     model = OnlineModel(ModelShape(layers=layers), dev)
     trace = spike_trace(seed, horizon, base, spike, period, width, prompt=prompt, output=output)
     warm_shapes(model, trace)
-    # A/B/A: standalone, colocated, standalone.  The colocated run is paired against the
-    # per-request mean of the two standalone runs (cancels clock/thermal drift), and the two
-    # standalone runs against each other give the A/A noise floor of the same statistic.
-    solo1 = Colocation(model, None, None).run(trace, horizon_s=horizon + 30)
-    pool = A.DevicePool(handles, 64, 16, device=device, slot_bytes=2 << 20, page_bytes=917504,
-                        max_requests=4096, max_pages_per_request=1024)
-    gate = A.Gate(device)
-    colo_rt = Colocation(model, pool, gate, offline_ctas=offline_ctas)
-    colo = colo_rt.run(trace, offline_population(seed, 4 * handles), horizon_s=horizon + 30)
-    solo2 = Colocation(model, None, None).run(trace, horizon_s=horizon + 30)
+    solos, colos = [], []
+    for i in range(repeats):
+        solos.append(Colocation(model, None, None).run(trace, horizon_s=horizon + 30))
+        pool = A.DevicePool(handles, 64, 16, device=device, slot_bytes=2 << 20, page_bytes=917504,
+                            max_requests=4096, max_pages_per_request=1024)
+        gate = A.Gate(device)
+        colo_rt = Colocation(model, pool, gate, offline_ctas=offline_ctas)
+        colos.append(colo_rt.run(trace, offline_population(seed, 4 * handles), horizon_s=horizon + 30))
+        del pool, gate, colo_rt
+        import gc
 
-    def avg(d1, d2):
-        return {k: (d1[k] + d2[k]) / 2 for k in d1 if k in d2}
+        gc.collect()  # the channel's ctypes hooks close over the runtime: break the cycle now
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+    solos.append(Colocation(model, None, None).run(trace, horizon_s=horizon + 30))
 
-    base_ttft, base_tpot = avg(solo1.ttft_us, solo2.ttft_us), avg(solo1.tpot_us, solo2.tpot_us)
-    ttft = paired_increase(base_ttft, colo.ttft_us)
-    tpot = paired_increase(base_tpot, colo.tpot_us)
-    aa_ttft = paired_increase(solo1.ttft_us, solo2.ttft_us)
-    aa_tpot = paired_increase(solo1.tpot_us, solo2.tpot_us)
+    base_ttft = _avg_runs([s.ttft_us for s in solos])
+    base_tpot = _avg_runs([s.tpot_us for s in solos])
+    colo_ttft = _avg_runs([c.ttft_us for c in colos])
+    colo_tpot = _avg_runs([c.tpot_us for c in colos])
+    ttft = paired_increase(base_ttft, colo_ttft)
+    tpot = paired_increase(base_tpot, colo_tpot)
+    even, odd = solos[0::2], solos[1::2]
+    aa_ttft = paired_increase(_avg_runs([s.ttft_us for s in even]), _avg_runs([s.ttft_us for s in odd]))
+    aa_tpot = paired_increase(_avg_runs([s.tpot_us for s in even]), _avg_runs([s.tpot_us for s in odd]))
+    mech_ttft = _avg_runs([c.mech_ttft_us for c in colos]) if colos else {}
+    mech_tpot = _avg_runs([c.mech_tpot_us for c in colos]) if colos else {}
+    colo = colos[-1]
 
     def mean(d):
         return sum(d.values()) / max(1, len(d))
@@ -500,34 +523,39 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         "trace": {"horizon_s": horizon, "online_requests": len(trace), "base_rate": base, "spike_rate": spike,
                   "period_s": period, "width_s": width, "prompt": list(prompt), "output": list(output),
                   "model": f"Llama-3-8B-shaped, {layers} layers, random init bf16"},
-        "design": "A/B/A: colocated paired against the per-request mean of two standalone runs",
+        "design": f"interleaved A/B x{repeats} + A: per-request mean over {repeats} colocated runs paired "
+                  f"against the per-request mean over {repeats + 1} standalone runs",
+        "repeats": repeats,
         "ttft_delta_pct": ttft["mean_pct"], "ttft_delta_max_pct": ttft["max_pct"],
         "tpot_delta_pct": tpot["mean_pct"], "tpot_delta_max_pct": tpot["max_pct"], "pairs": ttft["pairs"],
         "aa_noise_ttft_pct": aa_ttft["mean_pct"], "aa_noise_tpot_pct": aa_tpot["mean_pct"],
+        "per_run_ttft_delta_pct": [paired_increase(base_ttft, c.ttft_us)["mean_pct"] for c in colos],
+        "per_run_tpot_delta_pct": [paired_increase(base_tpot, c.tpot_us)["mean_pct"] for c in colos],
         # the reference DES's view of the same quantity: only the delays the mechanism puts on
         # the critical path (preempt wait + page acquisition/reclaim), per request, over the
         # standalone latency -- free of the run-to-run jitter of the end-to-end statistic
-        "ttft_attributable_pct": _attributable(colo.mech_ttft_us, base_ttft, 1),
-        "tpot_attributable_pct": _attributable(colo.mech_tpot_us, base_tpot,
+        "ttft_attributable_pct": _attributable(mech_ttft, base_ttft, 1),
+        "tpot_attributable_pct": _attributable(mech_tpot, base_tpot,
                                                {r.rid: max(1, r.output - 1) for r in trace}),
-        "preempt_wait_us": {"p50": _median(colo.quiesce_wait_us),
-                            "max": max(colo.quiesce_wait_us) if colo.quiesce_wait_us else None},
-        "ttft_ms": {"standalone": mean(base_ttft) / 1e3, "colocated": mean(colo.ttft_us) / 1e3},
-        "tpot_ms": {"standalone": mean(base_tpot) / 1e3, "colocated": mean(colo.tpot_us) / 1e3},
+        "preempt_wait_us": {"p50": _median([w for c in colos for w in c.quiesce_wait_us]),
+                            "max": max((w for c in colos for w in c.quiesce_wait_us), default=None)},
+        "ttft_ms": {"standalone": mean(base_ttft) / 1e3, "colocated": mean(colo_ttft) / 1e3},
+        "tpot_ms": {"standalone": mean(base_tpot) / 1e3, "colocated": mean(colo_tpot) / 1e3},
         "disables": colo.disables, "disables_per_request": colo.disables / max(1, len(trace)),
         "reclaims": colo.reclaims, "reclaimed_handles": colo.reclaimed_handles,
         "offline_ctas": offline_ctas or "default",
         "offline_gbs_harvested": colo.offline_bytes / colo.wall_s / 1e9,
-        "prefill_ms_median": {"standalone": _median(solo1.prefill_us + solo2.prefill_us) / 1e3,
-                              "colocated": _median(colo.prefill_us) / 1e3},
-        "decode_iter_ms_median": {"standalone": _median(solo1.decode_iter_us + solo2.decode_iter_us) / 1e3,
-                                  "colocated": _median(colo.decode_iter_us) / 1e3},
-        "wall_s": {"standalone": solo1.wall_s, "colocated": colo.wall_s},
+        "prefill_ms_median": {"standalone": _median([x for s in solos for x in s.prefill_us]) / 1e3,
+                              "colocated": _median([x for c in colos for x in c.prefill_us]) / 1e3},
+        "decode_iter_ms_median": {
+            "standalone": _median([x for s in solos for x in s.decode_iter_us]) / 1e3,
+            "colocated": _median([x for c in colos for x in c.decode_iter_us]) / 1e3},
+        "wall_s": {"standalone": solos[0].wall_s, "colocated": colo.wall_s},
     }
     import gc
 
-    del pool, gate, model, colo_rt
-    gc.collect()  # the channel's ctypes hooks close over the runtime: break the cycle now
+    del model, colos, solos
+    gc.collect()
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     return out

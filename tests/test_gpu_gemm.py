@@ -1,0 +1,119 @@
+"""Gated offline GEMM (tcgen05 + TMA, sm_100a): numerics against a torch fp32 reference of the same
+op, and the gate contract -- quiesce at tile granularity, resume from the HBM cursors, every
+128x256 tile computed exactly once across preemptions (bit-identical to an uninterrupted run).
+SURVEY §8f.2; work conservation as in SPEC.md:207 / test_sim.cpp:105-131."""
+import random
+import time
+
+import pytest
+
+from paper_2604_07874_b200 import api as A
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _operands(m, n, k, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    a = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
+    b = (torch.randn(n, k, device="cuda", generator=g) * 0.02).to(torch.bfloat16)  # N(0, 0.02) weights
+    return a, b
+
+
+def _run(gate, a, b, c, **kw):
+    gate.reset_work()
+    gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), a.shape[0], b.shape[0], a.shape[1], **kw)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 3584), (384, 1024, 1024), (512, 4608, 3584)])
+def test_gemm_matches_fp32_reference(m, n, k):
+    a, b = _operands(m, n, k, seed=m + n + k)
+    c = torch.full((m, n), float("nan"), dtype=torch.bfloat16, device="cuda")
+    gate = A.Gate(0)
+    _run(gate, a, b, c)
+    ref = a.float() @ b.float().t()
+    # fp32 accumulation, one bf16 rounding of the output: |err| <= 2^-8 |ref| (+ accumulation-order slack)
+    torch.testing.assert_close(c.float(), ref, rtol=8e-3, atol=2e-3 * ref.abs().max().item())
+    s = gate.read()
+    assert s.tiles_done == (m // 128) * (n // 256) and s.live_ctas == 0
+
+
+def test_gemm_ctas_fewer_than_tiles_and_no_poll():
+    m, n, k = 512, 2048, 512
+    a, b = _operands(m, n, k, seed=3)
+    gate = A.Gate(0)
+    c1 = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+    c2 = torch.empty_like(c1)
+    _run(gate, a, b, c1, ctas=3)
+    _run(gate, a, b, c2, poll=False)
+    assert torch.equal(c1, c2)  # same tile -> same bits, whatever CTA ran it
+
+
+def test_gemm_preempt_resume_conserves_tiles():
+    m, n, k = 2048, 4864, 3584  # 304 tiles of ~0.23 GFLOP
+    a, b = _operands(m, n, k, seed=7)
+    gate = A.Gate(0)
+    c_ref = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+    _run(gate, a, b, c_ref)
+    total = (m // 128) * (n // 256)
+    c = torch.full_like(c_ref, float("nan"))
+    gate.reset_work()
+    rng = random.Random(1)
+    gen = preemptions = 0
+    while True:
+        gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, ctas=4)
+        time.sleep(rng.uniform(0.0001, 0.0005))
+        gen += 1
+        gate.raise_(gen)
+        gate.wait_quiesced(gen)
+        torch.cuda.synchronize()
+        s = gate.read()
+        assert s.live_ctas == 0
+        assert s.tiles_done == min(s.tiles_claimed, total)  # claimed tiles all completed
+        gate.release(gen)
+        torch.cuda.synchronize()
+        preemptions += 1
+        if s.tiles_done >= total:
+            break
+        assert preemptions < 400
+    assert preemptions >= 2
+    assert torch.equal(c.view(torch.int16), c_ref.view(torch.int16))
+
+
+def test_gemm_quiesce_is_one_tile():
+    m, n, k = 8192, 18944, 3584  # Qwen2-7B gate/up projection over 8192 tokens: 4,736 tiles
+    a, b = _operands(m, n, k, seed=11)
+    c = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+    gate = A.Gate(0)
+    gs = torch.cuda.ExternalStream(gate.stream)
+    waits = []
+    for gen in range(1, 21):
+        gate.reset_work()
+        side = torch.cuda.Stream()
+        gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, stream=side.cuda_stream)
+        time.sleep(0.0003)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(gs)
+        gate.raise_(gen)
+        gate.wait_quiesced(gen)
+        e1.record(gs)
+        gate.release(gen)
+        torch.cuda.synchronize()
+        waits.append(e0.elapsed_time(e1) * 1e3)
+        assert gate.read().tiles_done < (m // 128) * (n // 256)  # it really was preempted
+    waits.sort()
+    # one 128x256x3584 tile is ~0.23 GFLOP (~15 us on one SM's tensor cores)
+    assert waits[len(waits) // 2] < 100.0, waits
+
+
+def test_gemm_rejects_bad_shapes():
+    gate = A.Gate(0)
+    a, b = _operands(128, 256, 64)
+    c = torch.empty((128, 256), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(A.InvalidArgument):
+        gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), 100, 256, 64)
+    with pytest.raises(A.InvalidArgument):
+        gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), 128, 256, 48)
+    with pytest.raises(A.InvalidArgument):
+        gate.launch_gemm(0, b.data_ptr(), c.data_ptr(), 128, 256, 64)

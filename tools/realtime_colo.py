@@ -17,6 +17,9 @@ if __name__ == "__main__":
     ap.add_argument("--spike", type=float, default=6.0)
     ap.add_argument("--handles", type=int, default=256)
     ap.add_argument("--seed", type=int, default=2604)
+    ap.add_argument("--repeats", type=int, default=2)
+    ap.add_argument("--offline-ctas", type=int, default=148)
     a = ap.parse_args()
     print(json.dumps(RT.measure_deltas(a.horizon, a.base, a.spike, handles=a.handles, layers=a.layers,
-                                       seed=a.seed)))
+                                       seed=a.seed, repeats=a.repeats,
+                                       offline_ctas=a.offline_ctas)))

@@ -168,6 +168,58 @@ def link_peak_d2h(torch, dev):
     return n / (best * 1e-3) / 1e9
 
 
+def gemm_tenant(torch, A, gate, dev, stream, gate_stream, preemptions, next_gen):
+    """The compute-bound offline tenant: Qwen2-7B gate/up projection (4096 tokens x 37888 x 3584)
+    on the gated tcgen05 GEMM -- TFLOP/s polled / unpolled / cuBLAS, and preempt-to-quiesce."""
+    m, n, k = 4096, 37888, 3584
+    a = torch.randn(m, k, device=dev).to(torch.bfloat16)
+    b = (torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16)
+    c = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+    flop = 2.0 * m * n * k
+
+    def timed(fn, reps=10):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    def run(poll):
+        gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, poll=poll,
+                         stream=stream.cuda_stream, fresh=True)
+
+    with torch.cuda.stream(stream):
+        t_poll, t_nopoll = timed(lambda: run(True)), timed(lambda: run(False))
+        t_cublas = timed(lambda: torch.matmul(a, b.t(), out=c))
+    q = []
+    total = (m // 128) * (n // 256)
+    for i in range(preemptions):
+        gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, stream=stream.cuda_stream, fresh=True)
+        time.sleep(0.0001 + 0.0004 * (i % 7) / 7)
+        gen = next_gen()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(gate_stream)
+        gate.raise_(gen)
+        gate.wait_quiesced(gen)
+        e1.record(gate_stream)
+        gate.release(gen)
+        torch.cuda.synchronize()
+        if gate.read().tiles_done < total:  # count only launches the raise really preempted
+            q.append(e0.elapsed_time(e1) * 1e3)
+    q.sort()
+    pick = (lambda p: round(q[min(len(q) - 1, int(round(p / 100 * (len(q) - 1))))], 2)) if q else (lambda p: None)
+    gate.reset_work()
+    return {"shape": [m, n, k], "tflops_polled": round(flop / t_poll / 1e9, 1),
+            "tflops_unpolled": round(flop / t_nopoll / 1e9, 1), "tflops_cublas": round(flop / t_cublas / 1e9, 1),
+            "polling_overhead_pct": round((t_poll / t_nopoll - 1) * 100, 2),
+            "preemptions": len(q), "p50_quiesce_us": pick(50), "p99_quiesce_us": pick(99),
+            "max_quiesce_us": q[-1] if q else None}
+
+
 def run_valve(args, rank, world, dist):
     import torch
 
@@ -320,6 +372,12 @@ def run_valve(args, rank, world, dist):
         polled = max(rates[True])
         unpolled = max(rates[False])
 
+    # ------------------------------------------------ GEMM tenant (tcgen05)
+    def next_gen():
+        gen[0] += 1
+        return gen[0]
+    gemm = gemm_tenant(torch, A, gate, dev, off_stream, gate_stream, 0 if args.profile_mode else 200, next_gen)
+
     # ------------------------------------------------ copy-engine alternative (same report)
     pool.reclaim(args.k, t + 5, 0)
     ce = pool.reclaim_copy(host.ptr, host.nbytes, engine="ce")
@@ -411,7 +469,8 @@ def run_valve(args, rank, world, dist):
 
         # offline harvest at one 8-warp CTA per SM (~3.7 TB/s of HBM reads in the gaps)
         rt = RT.measure_deltas(horizon=args.rt_horizon, device=gpu, seed=args.seed + rank, offline_ctas=148,
-                               repeats=args.rt_repeats)
+                               repeats=args.rt_repeats,
+                               log_dir=os.path.join(ROOT, "gpurun_out", "realtime_logs"))
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "r1_copy_traffic.json")))
     except OSError:
@@ -456,6 +515,7 @@ def run_valve(args, rank, world, dist):
         "step_quiesce_us_mean": round(statistics.mean(stats["quiesce_us"]), 1),
         "offline_polling_overhead_pct": round((1 - polled[0] / unpolled[0]) * 100, 2),
         "offline_gbs": {"polled": round(polled[0], 1), "unpolled": round(unpolled[0], 1)},
+        "offline_gemm": gemm,
         "policy_contrast_recompute": contrast,
         "ttft_delta_pct": rt.get("ttft_delta_pct"),
         "tpot_delta_pct": rt.get("tpot_delta_pct"),

@@ -25,6 +25,7 @@ constructs such a backend.
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import os
 from dataclasses import dataclass, field
 from typing import Callable, Dict, List, Optional, Sequence
@@ -175,7 +176,19 @@ def _arr(ctype, n):
 
 
 def _ptr(a, ctype):
+    if hasattr(a, "ctypes") and hasattr(a, "dtype"):  # numpy array
+        return a.ctypes.data_as(P(ctype))
     return C.cast(a, P(ctype))
+
+
+def _np():
+    import numpy
+
+    return numpy
+
+
+def _np_empty(n, dtype):
+    return _np().empty(max(int(n), 1), dtype=dtype)
 
 
 # ---------------------------------------------------------------------------- reclaim types
@@ -207,21 +220,21 @@ class ReclaimResult:
 
 
 def _csr(inst: ReclaimInstance):
-    n = len(inst.handles)
-    ids, mapped, off = _arr(C.c_int, n), _arr(i64, n), _arr(C.c_int, n + 1)
-    refs: List[int] = []
-    for i, h in enumerate(inst.handles):
-        ids[i], mapped[i], off[i] = int(h.id), int(h.mapped_at), len(refs)
-        refs.extend(int(r) for r in h.requests)
-    off[n] = len(refs)
-    reqs = _arr(i64, len(refs))
-    for i, r in enumerate(refs):
-        reqs[i] = r
+    np = _np()
+    hs = inst.handles
+    n = len(hs)
+    ids = np.fromiter((h.id for h in hs), np.int32, n) if n else _np_empty(0, np.int32)
+    mapped = np.fromiter((h.mapped_at for h in hs), np.int64, n) if n else _np_empty(0, np.int64)
+    off = np.zeros(n + 1, np.int32)
+    if n:
+        np.cumsum(np.fromiter((len(h.requests) for h in hs), np.int32, n), out=off[1:])
+    reqs = np.fromiter(itertools.chain.from_iterable(h.requests for h in hs), np.int64, int(off[n]))
+    if not len(reqs):
+        reqs = _np_empty(0, np.int64)
     keys = sorted(inst.cost)
     m = len(keys)
-    ck, cv = _arr(i64, m), _arr(i64, m)
-    for i, k in enumerate(keys):
-        ck[i], cv[i] = int(k), int(inst.cost[k])
+    ck = np.array(keys, np.int64) if m else _np_empty(0, np.int64)
+    cv = np.fromiter((inst.cost[k] for k in keys), np.int64, m) if m else _np_empty(0, np.int64)
     return n, ids, mapped, off, reqs, m, ck, cv
 
 
@@ -399,27 +412,27 @@ class MemoryPool:
         """memory.hpp:62 (costs attached by the caller)"""
         nh, nr = C.c_int(0), C.c_int(0)
         self._f("pool_snapshot", None, None, None, None, 0, 0, C.byref(nh), C.byref(nr))
-        ids, mapped = _arr(C.c_int, nh.value), _arr(i64, nh.value)
-        off, reqs = _arr(C.c_int, nh.value + 1), _arr(i64, nr.value)
+        np = _np()
+        ids, mapped = _np_empty(nh.value, np.int32), _np_empty(nh.value, np.int64)
+        off, reqs = _np_empty(nh.value + 1, np.int32), _np_empty(nr.value, np.int64)
         self._f("pool_snapshot", _ptr(ids, C.c_int), _ptr(mapped, i64), _ptr(off, C.c_int),
                 _ptr(reqs, i64), nh.value, nr.value, C.byref(nh), C.byref(nr))
+        n = nh.value
+        idl, mp, of, rq = ids[:n].tolist(), mapped[:n].tolist(), off[:n + 1].tolist(), reqs[:nr.value].tolist()
         inst = ReclaimInstance()
-        for i in range(nh.value):
-            inst.handles.append(ReclaimHandle(ids[i], mapped[i],
-                                              [reqs[j] for j in range(off[i], off[i + 1])]))
+        inst.handles = [ReclaimHandle(idl[i], mp[i], rq[of[i]:of[i + 1]]) for i in range(n)]
         return inst
 
     def apply_reclaim(self, handle_ids: Sequence[int], t: int) -> ReclaimResult:
         """memory.hpp:69-71"""
+        np = _np()
         k = len(handle_ids)
-        ids = _arr(C.c_int, k)
-        for i, h in enumerate(handle_ids):
-            ids[i] = int(h)
+        ids = np.array([int(h) for h in handle_ids], np.int32) if k else _np_empty(0, np.int32)
         cap_pages = self._total * self._hsz
         cap_ev = max(cap_pages, 1)
-        hs = _arr(C.c_int, max(k, self._total))
-        ev, off = _arr(i64, cap_ev), _arr(C.c_int, cap_ev + 1)
-        pg, ph, bl = _arr(i64, cap_pages), _arr(C.c_int, cap_pages), _arr(C.c_int, cap_pages)
+        hs = _np_empty(max(k, self._total), np.int32)
+        ev, off = _np_empty(cap_ev, np.int64), _np_empty(cap_ev + 1, np.int32)
+        pg, ph, bl = _np_empty(cap_pages, np.int64), _np_empty(cap_pages, np.int32), _np_empty(cap_pages, np.int32)
         nh, ne, npg = C.c_int(0), C.c_int(0), C.c_int(0)
         self._f("pool_apply_reclaim", _ptr(ids, C.c_int), k, int(t), _ptr(hs, C.c_int),
                 C.byref(nh), _ptr(ev, i64), C.byref(ne), _ptr(off, C.c_int), _ptr(pg, i64),
@@ -449,13 +462,21 @@ class MemoryPool:
 
 
 def _result(hs, nh, ev, ne, off, pg, ph, bl) -> ReclaimResult:
-    res = ReclaimResult([hs[i] for i in range(nh)], [ev[i] for i in range(ne)], {}, {}, {})
-    for i in range(ne):
-        req = ev[i]
-        rng = range(off[i], off[i + 1])
-        res.invalidated_pages[req] = [pg[j] for j in rng]
-        res.physical_pages[req] = [ph[j] for j in rng]
-        res.block_index[req] = [bl[j] for j in rng]
+    np = _np()
+
+    def lst(a, n):
+        a = a if isinstance(a, np.ndarray) else np.ctypeslib.as_array(a)
+        return a[:n].tolist()
+
+    evl, ofl = lst(ev, ne), lst(off, ne + 1)
+    npg = ofl[ne] if ne else 0
+    pgl, phl, bll = lst(pg, npg), lst(ph, npg), lst(bl, npg)
+    res = ReclaimResult(lst(hs, nh), evl, {}, {}, {})
+    for i, req in enumerate(evl):
+        a, b = ofl[i], ofl[i + 1]
+        res.invalidated_pages[req] = pgl[a:b]
+        res.physical_pages[req] = phl[a:b]
+        res.block_index[req] = bll[a:b]
     return res
 
 

@@ -10,7 +10,9 @@
 //                                    into a kStages-deep smem ring (full/empty mbarriers)
 //   warp 1 lane 0 : MMA issuer    -- 4 x tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256,
 //                                    K=16) per k-block, tcgen05.commit frees the smem stage
-//   warp 2        : TMEM owner    -- tcgen05.alloc / dealloc of 256 fp32 columns
+//   warp 2        : TMEM owner    -- tcgen05.alloc / dealloc of 2 x 256 fp32 columns (two
+//                                    accumulators: the epilogue of tile j overlaps the
+//                                    mainloop of tile j+1)
 //   warps 4..7    : epilogue      -- tcgen05.ld 32x32b.x32, bf16 pack, 16-byte global stores
 // Tiles (128 x 256 of C) are claimed from the gate's striped HBM cursors by thread 0 after reading the
 // gate word; a closed gate ends the loop, so the in-flight tile always completes (quiesce <= one
@@ -107,9 +109,10 @@ __global__ void __launch_bounds__(256, 1)
     k_offline_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    GemmArgs G) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[kGemmStages], empty_bar[kGemmStages], tmem_full;
+  __shared__ __align__(8) uint64_t full_bar[kGemmStages], empty_bar[kGemmStages];
+  __shared__ __align__(8) uint64_t tile_full[2], tile_empty[2], tmem_full[2], tmem_empty[2];
+  __shared__ long long s_tile[2];
   __shared__ uint32_t s_tmem;
-  __shared__ long long s_tile;
   // 1024-byte alignment for the swizzled operand tiles
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -118,14 +121,19 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(&tmem_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tile_full[s], 1);          // scheduler published the slot's tile id
+      mbar_init(&tile_empty[s], 1 + 128);   // MMA thread + 128 epilogue threads read it
+      mbar_init(&tmem_full[s], 1);          // tcgen05.commit: accumulator complete
+      mbar_init(&tmem_empty[s], 128);       // epilogue drained the accumulator
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
-                 "r"(kTmemCols));
+                 "r"(2 * kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_before();
@@ -134,14 +142,15 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem = s_tmem;
   const int tiles_n = G.n / kBN;
   const int kblocks = G.k / kBK;
-  uint32_t it0 = 0;  // k-blocks this CTA has streamed: the smem ring position of both roles
-  uint32_t acc_phase = 0;
   unsigned long long done = 0;
-  const unsigned long long total = (unsigned long long)G.total_tiles;
-  const unsigned long long per = (total + kStripes - 1) / kStripes;
-  int stripe = blockIdx.x % kStripes, visited = 0;  // thread 0 state (same claim order as decode)
-  for (;;) {
-    if (threadIdx.x == 0) {
+  if (warp == 0 && lane == 0) {
+    // ---------------- scheduler + TMA producer.  Tile j goes through smem slot j & 1; the
+    // producer runs at most one tile ahead of the epilogue (two accumulators in TMEM).
+    const unsigned long long total = (unsigned long long)G.total_tiles;
+    const unsigned long long per = (total + kStripes - 1) / kStripes;
+    int stripe = blockIdx.x % kStripes, visited = 0;
+    uint32_t it = 0;
+    for (uint32_t j = 0;; ++j) {
       long long t = -1;
       if (G.poll && ld_acquire(&G.g->closed)) {
         atomicCAS(&G.g->t_first_seen, 0ull, globaltimer_ns());
@@ -157,17 +166,14 @@ __global__ void __launch_bounds__(256, 1)
           ++visited;
         }
       }
-      s_tile = t;
-    }
-    __syncthreads();
-    const long long tile = s_tile;
-    if (tile < 0) break;
-    const int m0 = (int)(tile / tiles_n) * kBM;
-    const int n0 = (int)(tile % tiles_n) * kBN;
-    if (warp == 0 && lane == 0) {
-      // ---------------- TMA producer
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const uint32_t st = (it0 + kb) % kGemmStages, ph = ((it0 + kb) / kGemmStages) & 1u;
+      const uint32_t slot = j & 1, use = j >> 1;
+      mbar_wait(&tile_empty[slot], (use & 1) ^ 1);
+      s_tile[slot] = t;
+      mbar_arrive(&tile_full[slot]);
+      if (t < 0) break;
+      const int m0 = (int)(t / tiles_n) * kBM, n0 = (int)(t % tiles_n) * kBN;
+      for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        const uint32_t st = it % kGemmStages, ph = (it / kGemmStages) & 1u;
         mbar_wait(&empty_bar[st], ph ^ 1);
         uint8_t* sa = smem + st * kStageBytes;
         uint8_t* sb = sa + kABytes;
@@ -175,31 +181,51 @@ __global__ void __launch_bounds__(256, 1)
         tma_load_2d(sa, &map_a, &full_bar[st], kb * kBK, m0);
         tma_load_2d(sb, &map_b, &full_bar[st], kb * kBK, n0);
       }
-    } else if (warp == 1 && lane == 0) {
-      // ---------------- MMA issuer
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const uint32_t st = (it0 + kb) % kGemmStages, ph = ((it0 + kb) / kGemmStages) & 1u;
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer: accumulator j & 1 (TMEM columns 0 / 256)
+    uint32_t it = 0;
+    for (uint32_t j = 0;; ++j) {
+      const uint32_t slot = j & 1, use = j >> 1;
+      mbar_wait(&tile_full[slot], use & 1);
+      const long long t = s_tile[slot];
+      mbar_arrive(&tile_empty[slot]);
+      if (t < 0) break;
+      mbar_wait(&tmem_empty[slot], (use & 1) ^ 1);
+      fence_after();
+      const uint32_t acc = tmem + slot * kTmemCols;
+      for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        const uint32_t st = it % kGemmStages, ph = (it / kGemmStages) & 1u;
         mbar_wait(&full_bar[st], ph);
         fence_after();
         const uint32_t sa = smem_u32(smem + st * kStageBytes);
         const uint32_t sb = sa + kABytes;
 #pragma unroll
         for (int k = 0; k < kBK / kUK; ++k)
-          mma_bf16(tmem, smem_desc(sa + k * kUK * 2), smem_desc(sb + k * kUK * 2), (kb | k) != 0);
+          mma_bf16(acc, smem_desc(sa + k * kUK * 2), smem_desc(sb + k * kUK * 2), (kb | k) != 0);
         mma_commit(&empty_bar[st]);  // the stage is free once these MMAs have read it
       }
-      mma_commit(&tmem_full);  // accumulator complete
-    } else if (warp >= 4) {
-      // ---------------- epilogue: TMEM lanes 32*(warp-4).. -> rows of C
-      mbar_wait(&tmem_full, acc_phase);
+      mma_commit(&tmem_full[slot]);
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM lanes 32*(warp-4).. -> rows of C, overlapped with the
+    // next tile's mainloop in the other accumulator
+    const int q = warp - 4;
+    for (uint32_t j = 0;; ++j) {
+      const uint32_t slot = j & 1, use = j >> 1;
+      mbar_wait(&tile_full[slot], use & 1);
+      const long long t = s_tile[slot];
+      mbar_arrive(&tile_empty[slot]);
+      if (t < 0) break;
+      const int m0 = (int)(t / tiles_n) * kBM, n0 = (int)(t % tiles_n) * kBN;
+      mbar_wait(&tmem_full[slot], use & 1);
       fence_after();
-      const int q = warp - 4;
       const int row = m0 + q * 32 + lane;
       __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(G.c) + (int64_t)row * G.n + n0;
 #pragma unroll 1
       for (int c0 = 0; c0 < kBN; c0 += 32) {
         uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+        const uint32_t taddr = tmem + slot * kTmemCols + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
             "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -212,22 +238,21 @@ __global__ void __launch_bounds__(256, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         uint4* dst = reinterpret_cast<uint4*>(crow + c0);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          dst[j] = make_uint4(pack_bf16(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
-                              pack_bf16(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
-                              pack_bf16(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
-                              pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+        for (int jj = 0; jj < 4; ++jj)
+          dst[jj] = make_uint4(pack_bf16(__uint_as_float(v[8 * jj + 0]), __uint_as_float(v[8 * jj + 1])),
+                               pack_bf16(__uint_as_float(v[8 * jj + 2]), __uint_as_float(v[8 * jj + 3])),
+                               pack_bf16(__uint_as_float(v[8 * jj + 4]), __uint_as_float(v[8 * jj + 5])),
+                               pack_bf16(__uint_as_float(v[8 * jj + 6]), __uint_as_float(v[8 * jj + 7])));
       }
       fence_before();
+      mbar_arrive(&tmem_empty[slot]);
+      ++done;
     }
-    it0 += (uint32_t)kblocks;
-    acc_phase ^= 1;
-    ++done;
-    __syncthreads();  // TMEM drained before the next tile's first MMA overwrites it
-    fence_after();
   }
+  __syncthreads();
+  if (threadIdx.x == 128 && done) atomicAdd(&G.g->tiles_done, done);
+  __syncthreads();
   if (threadIdx.x == 0) {
-    if (done) atomicAdd(&G.g->tiles_done, done);
     __threadfence();
     if (atomicSub(&G.g->live_ctas, 1u) == 1u) {
       G.g->t_quiesced = globaltimer_ns();
@@ -237,7 +262,8 @@ __global__ void __launch_bounds__(256, 1)
   fence_before();
   __syncthreads();
   fence_after();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kTmemCols));
 }
 
 }  // namespace valve

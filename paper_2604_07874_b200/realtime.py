@@ -168,6 +168,43 @@ def spike_trace(seed: int, horizon_s: float, base_rate: float, spike_rate: float
     return out
 
 
+# ------------------------------------------------------------------------- event log
+
+class EventLog:
+    """The reference's events.jsonl schema (log.hpp:13-59, writer log.cpp:69-217): the same
+    kinds, field names and key order, so the reference's own build_report / ttft_increase /
+    tpot_increase (metrics.cpp:85-241) recompute the deltas from these logs (tests pin that)."""
+
+    def __init__(self):
+        self.recs = []
+
+    def add(self, t: int, kind: str, **fields):
+        self.recs.append((int(t), len(self.recs), kind, fields))
+
+    def records(self):
+        """Records in time order (ties keep emission order), sequence numbers reassigned."""
+        out = []
+        for seq, (t, _, kind, fields) in enumerate(sorted(self.recs, key=lambda r: (r[0], r[1]))):
+            out.append(dict(time_us=t, seq=seq, kind=kind, **fields))
+        return out
+
+    def write_jsonl(self, path: str):
+        import json
+
+        with open(path, "w") as f:
+            for r in self.records():
+                f.write(json.dumps(r, separators=(",", ":")) + "\n")
+
+
+def trace_fingerprint(trace: List["OnlineReq"]) -> str:
+    """A u64 of the online trace (arrival, prompt, output per request) -- pairs runs the way
+    the reference's online_fingerprint does (metrics.cpp:231-241 refuses unpaired logs)."""
+    import hashlib
+
+    h = hashlib.sha256(repr([(r.rid, r.arrival_us, r.prompt, r.output) for r in trace]).encode())
+    return "0x" + h.hexdigest()[:16]
+
+
 # ------------------------------------------------------------------------- the runtime
 
 @dataclass
@@ -187,6 +224,7 @@ class RunResult:
     # quiesce wait (CUDA events on the online stream) + page acquisition incl. reclaim (host)
     mech_ttft_us: Dict[int, float] = field(default_factory=dict)
     mech_tpot_us: Dict[int, float] = field(default_factory=dict)
+    log: EventLog = field(default_factory=EventLog)
 
 
 class Colocation:
@@ -222,6 +260,7 @@ class Colocation:
             (self.channel.handle_cooldown if cd else self.channel.handle_toggle)(when, gen)
 
     def _on_enabled(self, t):
+        self.res.log.add(t, "enable_issued", effective_us=int(t))
         self._launch_offline()
 
     def _launch_offline(self):
@@ -270,8 +309,15 @@ class Colocation:
                 self._reclaim(min(want, P.offline_handles()), now)
 
     def _reclaim(self, k, now):
+        op = self.res.reclaims
+        self.res.log.add(now, "reclaim_request", gpu=0, handles=int(k), op=op, purpose="shortfall")
+        t_r = time.perf_counter()
         nh, ne, npg = self.pool.reclaim(k, now)
         res = self.pool.last_reclaim()
+        self.res.log.add(now, "reclaim_done", gpu=0, op=op, latency_us=int((time.perf_counter() - t_r) * 1e6),
+                         handle_ids=list(res.handles))
+        for r in res.evicted_requests:
+            self.res.log.add(now, "evicted", request_id=int(r), gpu=0, recompute_tokens=int(self._off_cost.get(r, 0)))
         self.res.reclaims += 1
         self.res.reclaimed_handles += nh
         for r in res.evicted_requests:  # evicted-waiting -> re-admitted when memory frees
@@ -300,6 +346,12 @@ class Colocation:
         self._off_pages = 0
         self._harvest = 0
         reqs = [OnlineReq(r.rid, r.arrival_us, r.prompt, r.output) for r in trace]
+        log = self.res.log
+        log.add(0, "run_meta", scenario="realtime_spike", preset="valve" if self.colocated else "standalone",
+                seed=0, gpus=1, horizon_us=int(horizon_s * 1e6), online_fingerprint=trace_fingerprint(trace),
+                offline_fingerprint="0x%016x" % len(offline_reqs))
+        busy_since = 0
+        preempt_rids = []
         if self.colocated:
             P = self.pool
             P.online_grow(-(-P.total_handles() // 10), 0)
@@ -331,11 +383,15 @@ class Colocation:
             if self.colocated:
                 self._fire_timers(now)
             while nxt < len(reqs) and reqs[nxt].arrival_us <= now:
-                queue.append(reqs[nxt])
+                r = reqs[nxt]
+                log.add(r.arrival_us, "arrival", **{"class": "online"}, request_id=r.rid, gpu=0,
+                        prompt_tokens=r.prompt, output_tokens=r.output)
+                queue.append(r)
                 nxt += 1
             if not queue and not decoding:
                 if busy:  # idle edge (sim.cpp:371-380)
                     busy = False
+                    log.add(now, "busy", gpu=0, **{"class": "online"}, start_us=busy_since, end_us=now)
                     if self.colocated:
                         self.channel.note_all_idle(now)
                         self._readmit_offline(now)
@@ -349,7 +405,9 @@ class Colocation:
                 continue
             if not busy:  # busy edge: raise + wait for the offline CTAs to retire (sim.cpp:362-369)
                 busy = True
+                busy_since = now
                 if self.colocated:
+                    log.add(now, "disable_issued", effective_us=now, cause="busy")
                     self.channel.note_busy(now)
                     self._fire_timers(now)
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -367,15 +425,19 @@ class Colocation:
                     self.res.mech_ttft_us[r.rid] = (time.perf_counter() - ta) * 1e6
                     if pending_wait is not None:
                         wait_events.append((r.rid, pending_wait))
+                        preempt_rids.append((now, r.rid))
                         pending_wait = None
                 r.pages = need
                 caches[r.rid] = m.alloc()
                 toks = torch.randint(0, m.s.vocab, (r.prompt,), device=m.device)
                 t_it = now_us()
+                log.add(t_it, "prefill_start", **{"class": "online"}, request_id=r.rid, gpu=0, tokens=r.prompt)
                 m.prefill(toks, caches[r.rid])
                 lens[r.rid] = r.prompt
                 torch.cuda.synchronize()
-                self.res.prefill_us.append(now_us() - t_it)
+                t_pe = now_us()
+                log.add(t_pe, "prefill_end", **{"class": "online"}, request_id=r.rid, gpu=0)
+                self.res.prefill_us.append(t_pe - t_it)
                 decoding.append(r)
                 continue
             # one decode iteration over the batch
@@ -403,6 +465,7 @@ class Colocation:
                 r.emits.append(t_emit)
                 if len(r.emits) == 1:
                     r.first_us = t_emit
+                    log.add(t_emit, "first_token", **{"class": "online"}, request_id=r.rid, gpu=0)
                 if len(r.emits) == r.output:
                     done.append(r)
             for r in done:
@@ -413,10 +476,15 @@ class Colocation:
                 if r.output > 1:
                     self.res.tpot_us[r.rid] = (r.emits[-1] - r.emits[0]) / (r.output - 1)
                 self.res.ttft_us[r.rid] = r.first_us - r.arrival_us
+                log.add(t_emit, "done", **{"class": "online"}, request_id=r.rid, gpu=0, tokens=len(r.emits),
+                        first_token_us=r.emits[0], last_token_us=r.emits[-1], digest="0x0000000000000000")
         torch.cuda.synchronize()
         self.res.wall_s = time.perf_counter() - t0
-        for rid, (e0, e1) in wait_events:
+        if busy:
+            log.add(now_us(), "busy", gpu=0, **{"class": "online"}, start_us=busy_since, end_us=now_us())
+        for (t_adm, _), (rid, (e0, e1)) in zip(preempt_rids, wait_events):
             self.res.quiesce_wait_us.append(e0.elapsed_time(e1) * 1e3)
+            log.add(t_adm, "preempt_wait", gpu=0, request_id=rid, delay_us=int(round(self.res.quiesce_wait_us[-1])))
             self.res.mech_ttft_us[rid] = self.res.mech_ttft_us.get(rid, 0.0) + self.res.quiesce_wait_us[-1]
         if self.colocated:
             gen = self.channel.disables_issued() + 1000
@@ -471,8 +539,9 @@ def _avg_runs(dicts):
     return {k: sum(d[k] for d in dicts) / len(dicts) for k in sorted(keys)}
 
 
-def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, handles=256, seed=2604,
-                   output=(8, 12), prompt=(2500, 3500), layers=32, device=0, offline_ctas=0, repeats=1):
+def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, handles=64, seed=2604,
+                   output=(8, 12), prompt=(2500, 3500), layers=32, device=0, offline_ctas=0, repeats=1,
+                   log_dir: Optional[str] = None):
     """Paired standalone vs colocated run of one online trace (default: the pair_06 shape --
     spike base 0.3/s, 6/s for 1 s every 8 s, prompt 2500-3500, output 8-12 -- so the online
     lane goes idle and the offline tenant harvests the gaps).  Returns the reference's paired
@@ -482,7 +551,10 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
     ones): each request's latency is averaged over its standalone runs and over its colocated
     runs before pairing, which cancels clock/thermal drift and shrinks the batching-order jitter
     of a real-time loop by sqrt(repeats).  The A/A noise floor pairs the even standalone runs
-    against the odd ones (the same statistic with no mechanism in it)."""
+    against the odd ones (the same statistic with no mechanism in it).
+
+    log_dir: every run's events.jsonl in the reference schema (solo<i>.jsonl, colo<i>.jsonl), from
+    which the reference's own metrics code recomputes the paired deltas (tests/test_realtime_logs)."""
     dev = torch.device("cuda", device)
     model = OnlineModel(ModelShape(layers=layers), dev)
     trace = spike_trace(seed, horizon, base, spike, period, width, prompt=prompt, output=output)
@@ -502,6 +574,14 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
     solos.append(Colocation(model, None, None).run(trace, horizon_s=horizon + 30))
+    if log_dir:
+        import os
+
+        os.makedirs(log_dir, exist_ok=True)
+        for i, r in enumerate(solos):
+            r.log.write_jsonl(os.path.join(log_dir, f"solo{i}.jsonl"))
+        for i, r in enumerate(colos):
+            r.log.write_jsonl(os.path.join(log_dir, f"colo{i}.jsonl"))
 
     base_ttft = _avg_runs([s.ttft_us for s in solos])
     base_tpot = _avg_runs([s.tpot_us for s in solos])

@@ -15,7 +15,7 @@ if __name__ == "__main__":
     ap.add_argument("--horizon", type=float, default=24.0)
     ap.add_argument("--base", type=float, default=0.3)
     ap.add_argument("--spike", type=float, default=6.0)
-    ap.add_argument("--handles", type=int, default=256)
+    ap.add_argument("--handles", type=int, default=64)
     ap.add_argument("--seed", type=int, default=2604)
     ap.add_argument("--repeats", type=int, default=2)
     ap.add_argument("--offline-ctas", type=int, default=148)

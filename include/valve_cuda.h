@@ -102,6 +102,13 @@ int valve_pool_block_table(const valve_pool* p, int64_t req, int* out, int cap, 
 /* ------------------------------------------------- fused device reclaim (a2+a3+a5 on-device) */
 /* Recompute costs (requests.hpp:68-69, sim.cpp:877-883) kept next to each request row. */
 int valve_pool_set_costs(valve_pool* p, int n, const int64_t* reqs, const int64_t* costs);
+/* Per-request page size (C3: weight pages fill whole slots while a KV page of the offline model is
+ * page_bytes): 0 = the pool's page_bytes, else a 16-byte multiple <= slot_bytes.  Kept with the
+ * request row; reclaim reports, fill_pages, the gather copy and restore all honour it. */
+int valve_pool_set_page_bytes(valve_pool* p, int n, const int64_t* reqs, const int64_t* bytes);
+/* Destination layout of the last apply/reclaim report: total bytes the copy writes, and the page
+ * size of each evicted request (report order; request e's pages follow those of requests < e). */
+int valve_pool_last_copy_layout(const valve_pool* p, int64_t* page_bytes, int cap, int64_t* total);
 enum { VALVE_SELECT_SELECTIVE = 0, VALVE_SELECT_FIFO = 1, VALVE_SELECT_ORACLE = 2 };
 /* snapshot -> selection (mode) -> apply_reclaim in ONE kernel launch, no host round trip in
  * between (sim.cpp:936-942).  Results stay on the device for valve_pool_reclaim_copy();

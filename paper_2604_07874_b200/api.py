@@ -688,6 +688,8 @@ def _declare_valve_extras(L):
         "valve_pool_reclaim_copy_wait": (C.c_int, [vp, P(CopyStats)]),
         "valve_pool_reclaim_phases": (C.c_int, [vp, P(i64)]),
         "valve_pool_restore": (C.c_int, [vp, i64, vp, C.c_int, P(C.c_int), P(CopyParams), P(CopyStats)]),
+        "valve_pool_set_page_bytes": (C.c_int, [vp, C.c_int, P(i64), P(i64)]),
+        "valve_pool_last_copy_layout": (C.c_int, [vp, P(i64), C.c_int, P(i64)]),
         "valve_host_alloc": (C.c_int, [i64, P(vp)]),
         "valve_host_free": (None, [vp]),
         "valve_pool_fill_pages": (C.c_int, [vp]),
@@ -740,6 +742,28 @@ class DevicePool(MemoryPool):
         for i, (r, c) in enumerate(costs.items()):
             rq[i], cv[i] = int(r), int(c)
         self._b.check(self._b.lib.valve_pool_set_costs(self._h, n, _ptr(rq, i64), _ptr(cv, i64)))
+
+    def apply_reclaim(self, handle_ids: Sequence[int], t: int) -> ReclaimResult:
+        res = super().apply_reclaim(handle_ids, t)
+        self._last = (len(res.handles), len(res.evicted_requests),
+                      sum(len(v) for v in res.invalidated_pages.values()))
+        return res
+
+    def set_page_bytes(self, sizes: Dict[int, int]) -> None:
+        """Per-request page size (0 = the pool's page_bytes), e.g. whole-slot weight pages (C3)."""
+        n = len(sizes)
+        rq, bv = _arr(i64, n), _arr(i64, n)
+        for i, (r, b) in enumerate(sizes.items()):
+            rq[i], bv[i] = int(r), int(b)
+        self._b.check(self._b.lib.valve_pool_set_page_bytes(self._h, n, _ptr(rq, i64), _ptr(bv, i64)))
+
+    def last_copy_layout(self):
+        """(total destination bytes, page size of each evicted request in report order) of the
+        last apply_reclaim / reclaim: the copy writes request e's pages after those of e' < e."""
+        ne = self._last[1] if getattr(self, "_last", None) else 0
+        pb, tot = _arr(i64, max(ne, 1)), C.c_int64(0)
+        self._b.check(self._b.lib.valve_pool_last_copy_layout(self._h, _ptr(pb, i64), ne, C.byref(tot)))
+        return tot.value, [pb[i] for i in range(ne)]
 
     def reclaim(self, k: int, t: int, mode: int = 0):
         """Fused snapshot -> select -> apply on the device; returns (n_handles, n_evicted, n_pages)."""

@@ -47,26 +47,64 @@ __device__ __forceinline__ void pace(const CopyArgs& A, unsigned long long t0, l
 
 constexpr int kVec = 8;
 
+// Chunk prefix of a report with per-request page sizes: cbase[e] = sum over earlier evicted
+// requests of pages * ceil(page_bytes / chunk).
+__global__ void k_copy_plan(const int64_t* ev_pbytes, const int* inv_off, int n_ev, int64_t chunk,
+                            int64_t* cbase) {
+  int64_t carry = 0;
+  for (int base = 0; base < n_ev; base += blockDim.x) {
+    const int e = base + threadIdx.x;
+    const int64_t v = e < n_ev ? (int64_t)(inv_off[e + 1] - inv_off[e]) * ((ev_pbytes[e] + chunk - 1) / chunk) : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan64(v, tot);
+    if (e < n_ev) cbase[e] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) cbase[n_ev] = carry;
+}
+
 __global__ void __launch_bounds__(512) k_reclaim_copy(CopyArgs A) {
   __shared__ long long s_chunk;
   __shared__ unsigned long long s_t0;
+  __shared__ int64_t s_src, s_dst, s_len;
   if (threadIdx.x == 0) s_t0 = start_time(A.t_first);
   const int64_t cpp = (A.page_bytes + A.chunk_bytes - 1) / A.chunk_bytes;
+  const long long n_chunks = A.ev_cbase ? A.ev_cbase[A.n_ev] : A.n_chunks;
   for (;;) {
     if (threadIdx.x == 0) {
-      s_chunk = (long long)atomicAdd(A.cursor, 1ull);
-      if (s_chunk < A.n_chunks) pace(A, s_t0, s_chunk);
+      const long long c = (long long)atomicAdd(A.cursor, 1ull);
+      s_chunk = c;
+      if (c < n_chunks) {
+        pace(A, s_t0, c);
+        if (A.ev_cbase) {  // variable page sizes: locate the evicted request by its chunk prefix
+          int lo = 0, hi = A.n_ev - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (A.ev_cbase[mid] <= c) lo = mid;
+            else hi = mid - 1;
+          }
+          const int64_t pb = A.ev_pbytes[lo];
+          const int64_t cp = (pb + A.chunk_bytes - 1) / A.chunk_bytes;
+          const int64_t local = c - A.ev_cbase[lo];
+          const int64_t pg = local / cp, off = (local % cp) * A.chunk_bytes;
+          s_src = (int64_t)A.phys[A.inv_off[lo] + pg] * A.slot_bytes + off;
+          s_dst = A.ev_base[lo] + pg * pb + off;
+          s_len = min(A.chunk_bytes, pb - off);
+        } else {
+          const int64_t page = c / cpp, off = (c % cpp) * A.chunk_bytes;
+          s_src = (int64_t)A.phys[page] * A.slot_bytes + off;
+          s_dst = page * A.page_bytes + off;
+          s_len = min(A.chunk_bytes, A.page_bytes - off);
+        }
+      }
     }
     __syncthreads();
     const long long c = s_chunk;
+    const int64_t src_off = s_src, dst_off = s_dst, len = s_len;
     __syncthreads();
-    if (c >= A.n_chunks) break;
-    const int64_t page = c / cpp;
-    const int64_t off = (c % cpp) * A.chunk_bytes;
-    const int64_t len = min(A.chunk_bytes, A.page_bytes - off);
-    const uint4* src =
-        reinterpret_cast<const uint4*>(A.pages + (int64_t)A.phys[page] * A.slot_bytes + off);
-    uint4* dst = reinterpret_cast<uint4*>(A.dst + page * A.page_bytes + off);
+    if (c >= n_chunks) break;
+    const uint4* src = reinterpret_cast<const uint4*>(A.pages + src_off);
+    uint4* dst = reinterpret_cast<uint4*>(A.dst + dst_off);
     const int nvec = (int)(len >> 4);
     const int step = blockDim.x * kVec;
     for (int base = 0; base < nvec; base += step) {

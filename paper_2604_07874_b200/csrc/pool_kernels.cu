@@ -268,6 +268,7 @@ __global__ void k_offline_pages_of(PoolDev P, int64_t req) {
     const int row = ht_find(P, req);
     P.mirror->r[0] = row >= 0 ? P.row_npages[row] : 0;
     P.mirror->r[1] = row;
+    P.mirror->r[2] = row >= 0 && P.row_pbytes[row] ? P.row_pbytes[row] : P.page_bytes;
   }
   publish(P);
 }
@@ -397,10 +398,10 @@ __global__ void __launch_bounds__(kNT) k_check_invariants(PoolDev P, int64_t onl
 // Grid-stride over slots; 16-byte stores.
 __global__ void __launch_bounds__(256) k_fill_pages(PoolDev P) {
   const int64_t nslots = (int64_t)P.H * P.S;
-  const int64_t words = P.page_bytes / 8;
   for (int64_t p = blockIdx.x; p < nslots; p += gridDim.x) {
     const int row = P.slot_row[p];
     if (row < 0) continue;
+    const int64_t words = (P.row_pbytes[row] ? P.row_pbytes[row] : P.page_bytes) / 8;
     const uint64_t base = page_word_base(P.row_req[row], P.slot_blk[p]);
     ulonglong2* dst = reinterpret_cast<ulonglong2*>(P.pages + p * P.slot_bytes);
     for (int64_t w = threadIdx.x; w < words / 2; w += blockDim.x) {
@@ -412,8 +413,9 @@ __global__ void __launch_bounds__(256) k_fill_pages(PoolDev P) {
   }
 }
 
-// Recompute costs next to the request rows (sim.cpp:877-883 attaches them per snapshot).
-__global__ void k_set_costs(PoolDev P, int n, const int64_t* reqs, const int64_t* costs) {
+// Recompute costs next to the request rows (sim.cpp:877-883 attaches them per snapshot);
+// which = 1 sets the rows' page sizes instead (valve_pool_set_page_bytes).
+__global__ void k_set_costs(PoolDev P, int n, const int64_t* reqs, const int64_t* costs, int which) {
   __shared__ int s_missing;
   op_begin(P);
   if (threadIdx.x == 0) s_missing = 0;
@@ -421,7 +423,8 @@ __global__ void k_set_costs(PoolDev P, int n, const int64_t* reqs, const int64_t
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int row = ht_find(P, reqs[i]);
     if (row < 0) atomicAdd(&s_missing, 1);
-    else P.row_cost[row] = costs[i];
+    else if (which == 0) P.row_cost[row] = costs[i];
+    else P.row_pbytes[row] = costs[i];
   }
   __syncthreads();
   if (threadIdx.x == 0) P.mirror->r[0] = s_missing;

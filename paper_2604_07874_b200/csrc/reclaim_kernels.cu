@@ -494,6 +494,7 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
     for (int f = 0; f < ne; ++f) rank += P.row_req[P.s_evrows[f]] < req;
     P.s_rank[row] = rank;
     P.res_evicted[rank] = req;
+    P.res_ev_pbytes[rank] = P.row_pbytes[row] ? P.row_pbytes[row] : P.page_bytes;
   }
   __syncthreads();
   if (threadIdx.x == 0) g_apply_ns[1] = (long long)globaltimer_ns();
@@ -509,15 +510,31 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
   for (int i = threadIdx.x; i < nt; i += blockDim.x) atomicAdd(&bcnt[P.s_rank[P.s_qh[i]]], 1);
   __syncthreads();
   carry = 0;
+  int64_t bcarry = 0;
+  int custom = 0;
   for (int base = 0; base < ne; base += blockDim.x) {
     const int e = base + threadIdx.x;
     const int c = e < ne ? bcnt[e] : 0;
     int tot;
     const int ex = block_excl_scan(c, tot);
-    if (e < ne) P.res_inv_off[e] = carry + ex;
+    // destination byte layout of the copy: request e's pages at res_ev_base[e], pb bytes each
+    const int64_t pb = e < ne ? P.res_ev_pbytes[e] : 0;
+    int64_t btot;
+    const int64_t bex = block_excl_scan64((int64_t)c * pb, btot);
+    custom |= __syncthreads_or(e < ne && pb != P.page_bytes);
+    if (e < ne) {
+      P.res_inv_off[e] = carry + ex;
+      P.res_ev_base[e] = bcarry + bex;
+    }
     carry += tot;
+    bcarry += btot;
   }
-  if (threadIdx.x == 0) P.res_inv_off[ne] = nt;
+  if (threadIdx.x == 0) {
+    P.res_inv_off[ne] = nt;
+    P.res_ev_base[ne] = bcarry;
+    P.mirror->copy_bytes = bcarry;
+    P.mirror->copy_custom = custom;
+  }
   for (int e = threadIdx.x; e < ne; e += blockDim.x) bcnt[e] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < nt; i += blockDim.x) {

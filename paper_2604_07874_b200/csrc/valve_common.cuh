@@ -65,6 +65,9 @@ struct Mirror {
   int pad;
   int64_t err_arg;
   int64_t r[8];
+  int64_t copy_bytes;  // bytes the last apply/reclaim report asks the copy to move
+  int copy_custom;     // 1 if some evicted request has its own page size (set_page_bytes)
+  int pad2;
 };
 
 struct PoolDev {
@@ -78,6 +81,7 @@ struct PoolDev {
   int* slot_blk;
   int64_t* row_req;
   int64_t* row_cost;
+  int64_t* row_pbytes;  // per-row page size (0 = pool page_bytes), e.g. 2 MiB weight pages
   int* row_npages;
   int* row_nblk;
   int* bt;
@@ -115,6 +119,9 @@ struct PoolDev {
   int* res_phys;        // [H*S]
   int* res_blk;         // [H*S]
   int* res_counts;      // [4] n_handles, n_evicted, n_pages, err
+  int64_t* res_ev_pbytes;  // [R]   page size of each evicted request (report order)
+  int64_t* res_ev_base;    // [R+1] destination byte offset of each evicted request's pages
+  int64_t* res_ev_cbase;   // [R+1] copy-chunk prefix (per copy launch, variable-size path)
 };
 
 // ----------------------------------------------------------------------------- helpers
@@ -163,6 +170,33 @@ __device__ __forceinline__ int block_excl_scan(int v, int& total) {
   __syncthreads();
   const int base = wid ? ws[wid - 1] : 0;
   total = ws[nw - 1];
+  __syncthreads();
+  return base + inc - v;
+}
+
+__device__ __forceinline__ int64_t block_excl_scan64(int64_t v, int64_t& total) {
+  __shared__ int64_t ws64x[33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t n = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += n;
+  }
+  if (lane == 31) ws64x[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t x = lane < nw ? ws64x[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t n = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += n;
+    }
+    ws64x[lane] = x;
+  }
+  __syncthreads();
+  const int64_t base = wid ? ws64x[wid - 1] : 0;
+  total = ws64x[nw - 1];
   __syncthreads();
   return base + inc - v;
 }
@@ -302,6 +336,7 @@ __device__ __forceinline__ int ht_insert(const PoolDev& P, int64_t key) {
   P.ht_row[i] = row;
   P.row_req[row] = key;
   P.row_cost[row] = 0;
+  P.row_pbytes[row] = 0;
   P.row_npages[row] = 0;
   P.row_nblk[row] = 0;
   return row;

@@ -120,6 +120,8 @@ struct valve_pool {
   size_t smem_snapshot = 0, smem_reclaim = 0;
   std::vector<void*> dev_allocs;
   int last_n_handles = 0, last_n_evicted = 0, last_n_pages = 0;
+  int64_t last_copy_bytes = 0;  // destination bytes of the last report (per-request page sizes)
+  int last_custom = 0;          // some evicted request has its own page size
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaStream_t copy_stream = nullptr;  // reclaim copies overlap pool bookkeeping
   cudaEvent_t ev_report = nullptr;
@@ -251,6 +253,7 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   d.slot_blk = p->dalloc<int>(HS);
   d.row_req = p->dalloc<int64_t>(R);
   d.row_cost = p->dalloc<int64_t>(R);
+  d.row_pbytes = p->dalloc<int64_t>(R);
   d.row_npages = p->dalloc<int>(R);
   d.row_nblk = p->dalloc<int>(R);
   d.bt = p->dalloc<int>((int64_t)R * p->Pblk);
@@ -284,6 +287,9 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   d.res_phys = p->dalloc<int>(HS);
   d.res_blk = p->dalloc<int>(HS);
   d.res_counts = p->dalloc<int>(4);
+  d.res_ev_pbytes = p->dalloc<int64_t>(R);
+  d.res_ev_base = p->dalloc<int64_t>(R + 1);
+  d.res_ev_cbase = p->dalloc<int64_t>(R + 1);
   p->d_ids = p->dalloc<int>(std::max(std::max(H, 1) * 2, p->Pblk));
   p->d_in64 = p->dalloc<int64_t>(R);
   p->d_in64b = p->dalloc<int64_t>(R);
@@ -308,6 +314,7 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   ck(cudaMemsetAsync(d.row_npages, 0, R * 4, p->stream), "memset");
   ck(cudaMemsetAsync(d.row_nblk, 0, R * 4, p->stream), "memset");
   ck(cudaMemsetAsync(d.row_cost, 0, R * 8, p->stream), "memset");
+  ck(cudaMemsetAsync(d.row_pbytes, 0, R * 8, p->stream), "memset");
   ck(cudaMemsetAsync(d.bt, 0xff, (size_t)R * p->Pblk * 4, p->stream), "memset");
   ck(cudaMemsetAsync(d.ht_row, 0xff, (size_t)d.HC * 4, p->stream), "memset");
   ck(cudaMemsetAsync(d.s_ev, 0, R * 4, p->stream), "memset");
@@ -531,11 +538,15 @@ int valve_pool_apply_reclaim(valve_pool* p, const int* ids, int k, int64_t t, in
       p->last_n_handles = (int)p->mirror->r[0];
       p->last_n_evicted = (int)p->mirror->r[1];
       p->last_n_pages = (int)p->mirror->r[2];
+    p->last_copy_bytes = p->mirror->copy_bytes;
+    p->last_custom = p->mirror->copy_custom;
       throw;
     }
     p->last_n_handles = (int)p->mirror->r[0];
     p->last_n_evicted = (int)p->mirror->r[1];
     p->last_n_pages = (int)p->mirror->r[2];
+    p->last_copy_bytes = p->mirror->copy_bytes;
+    p->last_custom = p->mirror->copy_custom;
   });
   if (n_handles) *n_handles = p->last_n_handles;
   if (n_evicted) *n_evicted = p->last_n_evicted;
@@ -586,8 +597,36 @@ int valve_pool_set_costs(valve_pool* p, int n, const int64_t* reqs, const int64_
     ck(cudaMemcpyAsync(p->d_in64, reqs, (size_t)n * 8, cudaMemcpyHostToDevice, p->stream), "upload");
     ck(cudaMemcpyAsync(p->d_in64b, costs, (size_t)n * 8, cudaMemcpyHostToDevice, p->stream), "upload");
     p->launch1("set_costs", k_set_costs, 0, p->d, n, (const int64_t*)p->d_in64,
-               (const int64_t*)p->d_in64b);
+               (const int64_t*)p->d_in64b, 0);
     if (p->mirror->r[0]) fail(VALVE_INVALID_ARGUMENT, "set_costs: request has no live pages in the pool");
+  });
+}
+
+int valve_pool_set_page_bytes(valve_pool* p, int n, const int64_t* reqs, const int64_t* bytes) {
+  return guard([&] {
+    if (n < 0 || n > p->R) fail(VALVE_INVALID_ARGUMENT, "set_page_bytes: bad count");
+    for (int i = 0; i < n; ++i)
+      if (bytes[i] < 0 || bytes[i] > p->d.slot_bytes || bytes[i] % 16 || (bytes[i] && !p->d.pages))
+        fail(VALVE_INVALID_ARGUMENT, "set_page_bytes: need 0 or a 16-byte multiple <= slot_bytes");
+    if (!n) return;
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    ck(cudaMemcpyAsync(p->d_in64, reqs, (size_t)n * 8, cudaMemcpyHostToDevice, p->stream), "upload");
+    ck(cudaMemcpyAsync(p->d_in64b, bytes, (size_t)n * 8, cudaMemcpyHostToDevice, p->stream), "upload");
+    p->launch1("set_page_bytes", k_set_costs, 0, p->d, n, (const int64_t*)p->d_in64,
+               (const int64_t*)p->d_in64b, 1);
+    if (p->mirror->r[0]) fail(VALVE_INVALID_ARGUMENT, "set_page_bytes: request has no live pages in the pool");
+  });
+}
+
+int valve_pool_last_copy_layout(const valve_pool* cp, int64_t* page_bytes, int cap, int64_t* total) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] {
+    if (total) *total = p->last_copy_bytes;
+    if (page_bytes && p->last_n_evicted) {
+      ck(cudaMemcpyAsync(page_bytes, p->d.res_ev_pbytes, (size_t)std::min(cap, p->last_n_evicted) * 8,
+                         cudaMemcpyDeviceToHost, p->stream), "read");
+      ck(cudaStreamSynchronize(p->stream), "read");
+    }
   });
 }
 
@@ -602,6 +641,8 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
     p->last_n_handles = (int)p->mirror->r[0];
     p->last_n_evicted = (int)p->mirror->r[1];
     p->last_n_pages = (int)p->mirror->r[2];
+    p->last_copy_bytes = p->mirror->copy_bytes;
+    p->last_custom = p->mirror->copy_custom;
     if (n_handles) *n_handles = p->last_n_handles;
     if (n_evicted) *n_evicted = p->last_n_evicted;
     if (n_pages) *n_pages = p->last_n_pages;
@@ -682,10 +723,11 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
     if (c.chunk_bytes % 16 || c.threads % 32 || c.threads > 512)
       fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: chunk must be a 16-byte multiple, threads <= 512");
     if (p->copy_pending) fail(VALVE_LOGIC_ERROR, "reclaim_copy: a copy is already in flight");
-    const int64_t need = (int64_t)p->last_n_pages * p->d.page_bytes;
+    const int64_t need = p->last_copy_bytes;
     if (dst_bytes < need) fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: destination too small");
     if (reinterpret_cast<uintptr_t>(host_dst) % 16)
       fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: destination must be 16-byte aligned");
+    const bool custom = p->last_custom != 0;
     ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
     void* ddst = nullptr;
     ck(cudaHostGetDevicePointer(&ddst, host_dst, 0),
@@ -711,9 +753,21 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
     ck(cudaEventRecord(p->ev_report, p->stream), "event");
     ck(cudaStreamWaitEvent(p->copy_stream, p->ev_report, 0), "event wait");
     ck(cudaMemsetAsync(ctr, 0, 24, p->copy_stream), "memset");
+    if (custom) {  // per-request page sizes: chunk prefix over the evicted requests first
+      A.ev_pbytes = p->d.res_ev_pbytes;
+      A.ev_base = p->d.res_ev_base;
+      A.ev_cbase = p->d.res_ev_cbase;
+      A.inv_off = p->d.res_inv_off;
+      A.n_ev = p->last_n_evicted;
+      A.n_chunks = p->last_n_evicted > 0 ? 1 : 0;  // the kernel reads the total from ev_cbase
+      if (A.n_chunks) {
+        k_copy_plan<<<1, 1024, 0, p->copy_stream>>>(A.ev_pbytes, A.inv_off, A.n_ev, A.chunk_bytes, p->d.res_ev_cbase);
+        counted();
+      }
+    }
     ck(cudaEventRecord(p->ev0, p->copy_stream), "event");
     if (A.n_chunks > 0) {
-      if (c.use_tma) {
+      if (c.use_tma && !custom) {
         k_reclaim_copy_tma<<<c.ctas, 32, 2 * 32768, p->copy_stream>>>(A);
       } else {
         k_reclaim_copy<<<c.ctas, c.threads, 0, p->copy_stream>>>(A);
@@ -779,6 +833,7 @@ int valve_pool_restore(valve_pool* p, int64_t req, const void* host_src, int n_p
     counted();
     p->sync_and_check("restore");
     const int row = (int)p->mirror->r[1];
+    const int64_t pb = p->mirror->r[2];  // the request's page size (set_page_bytes or the pool's)
     if (row < 0) fail(VALVE_LOGIC_ERROR, "restore: request holds no pages (reserve it first)");
     if (n_pages == 0) return;
     const void* dsrc = nullptr;
@@ -789,7 +844,7 @@ int valve_pool_restore(valve_pool* p, int64_t req, const void* host_src, int n_p
     ScatterArgs A{};
     A.pages = p->d.pages;
     A.slot_bytes = p->d.slot_bytes;
-    A.page_bytes = p->d.page_bytes;
+    A.page_bytes = pb;
     A.chunk_bytes = c.chunk_bytes;
     A.bt_row = p->d.bt + (int64_t)row * p->Pblk;
     A.nblk = p->d.row_nblk + row;
@@ -813,7 +868,7 @@ int valve_pool_restore(valve_pool* p, int64_t req, const void* host_src, int n_p
     if (st) {
       float ms = 0;
       ck(cudaEventElapsedTime(&ms, p->ev0, p->ev1), "event");
-      st->bytes = (int64_t)n_pages * p->d.page_bytes;
+      st->bytes = (int64_t)n_pages * pb;
       st->pages = n_pages;
       st->kernel_ms = ms;
       st->t_first_ns = st->t_last_ns = 0;
@@ -835,19 +890,35 @@ void valve_host_free(void* p) {
 int valve_pool_reclaim_copy_ce(valve_pool* p, void* host_dst, int64_t dst_bytes, valve_copy_stats* st) {
   return guard([&] {
     if (!p->d.pages) fail(VALVE_LOGIC_ERROR, "reclaim_copy: pool has no page store");
-    const int64_t need = (int64_t)p->last_n_pages * p->d.page_bytes;
+    const int64_t need = p->last_copy_bytes;
     if (dst_bytes < need) fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: destination too small");
     ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    p->order_after_copy();
     std::vector<int> phys(p->last_n_pages);
+    std::vector<size_t> sizes(phys.size(), (size_t)p->d.page_bytes);
+    std::vector<size_t> offs(phys.size());
     if (!phys.empty()) {
       ck(cudaMemcpyAsync(phys.data(), p->d.res_phys, phys.size() * 4, cudaMemcpyDeviceToHost, p->stream), "read");
+      std::vector<int64_t> pb(p->last_n_evicted), base(p->last_n_evicted + 1);
+      std::vector<int> io(p->last_n_evicted + 1);
+      if (p->last_custom) {
+        ck(cudaMemcpyAsync(pb.data(), p->d.res_ev_pbytes, pb.size() * 8, cudaMemcpyDeviceToHost, p->stream), "read");
+        ck(cudaMemcpyAsync(base.data(), p->d.res_ev_base, base.size() * 8, cudaMemcpyDeviceToHost, p->stream), "read");
+        ck(cudaMemcpyAsync(io.data(), p->d.res_inv_off, io.size() * 4, cudaMemcpyDeviceToHost, p->stream), "read");
+      }
       ck(cudaStreamSynchronize(p->stream), "read");
+      for (size_t i = 0; i < phys.size(); ++i) offs[i] = i * (size_t)p->d.page_bytes;
+      if (p->last_custom)
+        for (int e = 0; e < p->last_n_evicted; ++e)
+          for (int j = io[e]; j < io[e + 1]; ++j) {
+            sizes[j] = (size_t)pb[e];
+            offs[j] = (size_t)(base[e] + (int64_t)(j - io[e]) * pb[e]);
+          }
     }
     // one batched copy-engine submission (CUDA >= 12.8); per-page copies if unsupported
     std::vector<void*> dsts(phys.size()), srcs(phys.size());
-    std::vector<size_t> sizes(phys.size(), (size_t)p->d.page_bytes);
     for (size_t i = 0; i < phys.size(); ++i) {
-      dsts[i] = static_cast<uint8_t*>(host_dst) + i * p->d.page_bytes;
+      dsts[i] = static_cast<uint8_t*>(host_dst) + offs[i];
       srcs[i] = p->d.pages + (int64_t)phys[i] * p->d.slot_bytes;
     }
     cudaMemcpyAttributes attr{};

@@ -38,7 +38,7 @@ __global__ void k_apply(PoolDev P, const int* ids, int k, int64_t t);
 __global__ void k_reclaim(PoolDev P, int k, int mode, int64_t t);
 __global__ void k_check_invariants(PoolDev P, int64_t online_used);
 __global__ void k_fill_pages(PoolDev P);
-__global__ void k_set_costs(PoolDev P, int n, const int64_t* reqs, const int64_t* costs);
+__global__ void k_set_costs(PoolDev P, int n, const int64_t* reqs, const int64_t* costs, int which);
 __global__ void k_select_instance(SelectArgs A);
 __global__ void k_map_refs(const int64_t* reqs, int nnz, const int64_t* keys, int m, int* rref);
 __global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix,
@@ -60,8 +60,16 @@ struct CopyArgs {
   unsigned long long* cursor;
   unsigned long long* t_first;
   unsigned long long* t_last;
+  // variable page sizes (some request has set_page_bytes): ev_cbase != nullptr
+  const int64_t* ev_pbytes;  // page size per evicted request
+  const int64_t* ev_base;    // destination byte offset per evicted request
+  const int64_t* ev_cbase;   // chunk prefix per evicted request [n_ev + 1]
+  const int* inv_off;        // first report page of each evicted request
+  int n_ev;
 };
 __global__ void k_reclaim_copy(CopyArgs A);
+__global__ void k_copy_plan(const int64_t* ev_pbytes, const int* inv_off, int n_ev, int64_t chunk,
+                            int64_t* cbase);
 __global__ void k_reclaim_copy_tma(CopyArgs A);
 
 // restore scatter (copy_kernels.cu): host pages back into a request's (re-reserved) slots

@@ -281,3 +281,98 @@ def test_restore_rejects_bad_blocks():
         pool.restore(5, buf.ptr, [3])  # block 3 is not mapped (3 pages)
     pool.restore(5, buf.ptr, [2, 0, 1])
     pool.check_invariants()
+
+
+def _expected_images_var(oracle_c, res, sizes, default):
+    """Byte images of a report with per-request page sizes: request e's pages (its own size)
+    follow those of the earlier evicted requests."""
+    parts = []
+    for r in res.evicted_requests:
+        blks = res.block_index[r]
+        n = len(blks)
+        pb = sizes.get(r, default)
+        out = np.zeros(max(n, 1) * pb, dtype=np.uint8)
+        rq = (C.c_int64 * max(n, 1))(*([r] * n))
+        bk = (C.c_int32 * max(n, 1))(*blks)
+        oracle_c.lib.vo_gather_images(rq, bk, n, pb, out.ctypes.data)
+        parts.append(out[: n * pb])
+    return np.concatenate(parts) if parts else np.zeros(0, np.uint8)
+
+
+@pytest.mark.parametrize("engine,kw", [
+    ("sm", dict(ctas=6, chunk_bytes=8192)),
+    ("sm", dict(ctas=2, chunk_bytes=65536)),
+    ("sm", dict(ctas=4, use_tma=1, chunk_bytes=8192)),  # variable sizes take the LDG/STG kernel
+    ("ce", {}),
+])
+def test_weight_pages_fill_whole_slots(oracle_c, engine, kw):
+    """C3 geometry in miniature: offline KV pages of page_bytes and weight pages that fill the
+    whole slot, reclaimed together; the copy lays each request's pages out at its own size."""
+    rng = random.Random(21)
+    slot, page = 65536, 49152
+    H, S = 24, 8
+    pool = A.DevicePool(H, S, 16, slot_bytes=slot, page_bytes=page)
+    weights = {2_000_000 + layer: 11 for layer in range(3)}  # three "layers" of 11 slots
+    for w, n in weights.items():
+        assert pool.offline_reserve(w, n, 0)
+    kv = [r for r in range(40) if pool.offline_reserve(r, rng.randint(1, 6), 1)]
+    sizes = {w: slot for w in weights}
+    pool.set_page_bytes(sizes)
+    pool.fill_pages()
+    pool.set_costs({**{w: 10**9 for w in weights}, **{r: rng.randint(1, 100) for r in kv}})
+    ids = sorted(set(pool.handles_of_request(2_000_001)) | set(pool.handles_of_request(0)))
+    res = pool.apply_reclaim(ids, 10)
+    assert 2_000_001 in res.evicted_requests
+    total, pbs = pool.last_copy_layout()
+    assert pbs == [sizes.get(r, page) for r in res.evicted_requests]
+    want = _expected_images_var(oracle_c, res, sizes, page)
+    assert total == len(want)
+    buf = A.HostBuffer(total)
+    st = pool.reclaim_copy(buf.ptr, buf.nbytes, A.copy_params(**kw) if kw else None, engine=engine)
+    assert st.bytes == total
+    assert np.array_equal(buf.view(), want)
+    # the fused device reclaim reports the same layout
+    pool.online_release(len(res.handles))
+    t, n = 20, pool.reclaim(6, 20)
+    res2 = pool.last_reclaim()
+    total2, _ = pool.last_copy_layout()
+    buf2 = A.HostBuffer(max(total2, 16))
+    pool.reclaim_copy(buf2.ptr, buf2.nbytes, A.copy_params(ctas=3, chunk_bytes=16384))
+    assert np.array_equal(buf2.view()[:total2], _expected_images_var(oracle_c, res2, sizes, page))
+
+
+def test_weight_restore_uses_request_page_size(oracle_c):
+    slot, page = 65536, 49152
+    pool = A.DevicePool(16, 8, 16, slot_bytes=slot, page_bytes=page)
+    W = 7_000_000
+    assert pool.offline_reserve(W, 13, 0)
+    pool.set_page_bytes({W: slot})
+    pool.fill_pages()
+    res = pool.apply_reclaim(sorted(pool.handles_of_request(W)), 5)
+    total, _ = pool.last_copy_layout()
+    assert total == 13 * slot
+    buf = A.HostBuffer(total)
+    pool.reclaim_copy(buf.ptr, buf.nbytes)
+    pool.online_release(len(res.handles))
+    assert pool.offline_reserve(W, 13, 6)
+    pool.set_page_bytes({W: slot})
+    order = res.block_index[W]
+    st = pool.restore(W, buf.ptr, order)
+    assert st.bytes == 13 * slot
+    res2 = pool.apply_reclaim(sorted(pool.handles_of_request(W)), 7)
+    buf2 = A.HostBuffer(13 * slot)
+    pool.reclaim_copy(buf2.ptr, buf2.nbytes)
+    assert np.array_equal(buf2.view(), _expected_images_var(oracle_c, res2, {W: slot}, page))
+
+
+def test_set_page_bytes_validation():
+    pool = A.DevicePool(8, 4, 16, slot_bytes=8192, page_bytes=4096)
+    assert pool.offline_reserve(1, 2, 0)
+    with pytest.raises(A.InvalidArgument):
+        pool.set_page_bytes({1: 8192 + 16})
+    with pytest.raises(A.InvalidArgument):
+        pool.set_page_bytes({1: 100})
+    with pytest.raises(A.InvalidArgument):
+        pool.set_page_bytes({99: 4096})  # no live pages
+    pool.set_page_bytes({1: 8192})
+    pool.set_page_bytes({1: 0})

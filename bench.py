@@ -168,6 +168,75 @@ def link_peak_d2h(torch, dev):
     return n / (best * 1e-3) / 1e9
 
 
+def link_peak_h2d(torch, dev):
+    n = 256 << 20
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    best = 1e9
+    for _ in range(8):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        d.copy_(h, non_blocking=True)
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e))
+    return n / (best * 1e-3) / 1e9
+
+
+def c3_weights(torch, A, gpu, cp, seed, d2h_peak):
+    """BASELINE configs[2] (C3) mechanism at real geometry: Qwen2-7B weights as reclaimable
+    residents -- 28 layers x 260 whole-slot (2 MiB) pages = 7,280 slots (15.3 GB, ~114 handles) --
+    next to offline KV on a 256-handle (32 GiB) pool.  One op evicts 4 layers' handles (their
+    co-resident KV goes too): gather to host at each request's own page size, then the layers are
+    re-reserved and scattered back (k_restore_scatter).  GB/s against the measured link peaks."""
+    H = 256
+    pool = A.DevicePool(H, HSZ, 16, device=gpu, slot_bytes=SLOT, page_bytes=PAGE, max_requests=4096,
+                        max_pages_per_request=1024)
+    pool.online_grow(-(-H // 10), 0)
+    layers = {3_000_000 + i: 260 for i in range(28)}
+    for w, n in layers.items():
+        assert pool.offline_reserve(w, n, 0)
+    pool.set_page_bytes({w: SLOT for w in layers})
+    live, t = populate(pool, offline_requests(seed, 4 * H))
+    pool.set_costs({**{w: 10**12 for w in layers}, **{r: c for r, (p, c) in live.items()}})
+    pool.fill_pages()
+    out = {"pool_handles": H, "weight_layers": len(layers), "weight_pages": sum(layers.values()),
+           "weight_gb": round(sum(layers.values()) * SLOT / 1e9, 2), "ops": []}
+    h2d_peak = link_peak_h2d(torch, torch.device("cuda", gpu))
+    for op, first in enumerate((0, 8, 16)):
+        evict = list(layers)[first:first + 4]
+        ids = sorted(set().union(*[set(pool.handles_of_request(w)) for w in evict]))
+        t += 10
+        res = pool.apply_reclaim(ids, t)
+        total, pbs = pool.last_copy_layout()
+        host = A.HostBuffer(total)
+        st = pool.reclaim_copy(host.ptr, host.nbytes, cp)
+        pool.online_release(len(res.handles))
+        base, rest_bytes, rest_ms = 0, 0, 0.0
+        for r, pb in zip(res.evicted_requests, pbs):
+            n = len(res.invalidated_pages[r])
+            if r in layers:
+                t += 1
+                assert pool.offline_reserve(r, layers[r], t)
+                pool.set_page_bytes({r: SLOT})
+                rs = pool.restore(r, host.ptr + base, res.block_index[r], A.copy_params(ctas=32))
+                rest_bytes += rs.bytes
+                rest_ms += rs.kernel_ms
+            base += n * pb
+        weights = sum(len(res.invalidated_pages[w]) for w in evict) * SLOT
+        out["ops"].append({"handles": len(res.handles), "evicted_requests": len(res.evicted_requests),
+                           "bytes": total, "weight_bytes": weights, "copy_gbs": round(st.bytes / st.kernel_ms / 1e6, 2),
+                           "restore_gbs": round(rest_bytes / rest_ms / 1e6, 2) if rest_ms else None})
+        del host
+    gb = [o["copy_gbs"] for o in out["ops"]]
+    rb = [o["restore_gbs"] for o in out["ops"] if o["restore_gbs"]]
+    out.update({"copy_gbs": round(statistics.mean(gb), 2), "copy_frac_d2h": round(statistics.mean(gb) / d2h_peak, 4),
+                "restore_gbs": round(statistics.mean(rb), 2) if rb else None, "h2d_peak_gbs": round(h2d_peak, 2),
+                "restore_frac_h2d": round(statistics.mean(rb) / h2d_peak, 4) if rb else None})
+    del pool
+    return out
+
+
 def gemm_tenant(torch, A, gate, dev, stream, gate_stream, preemptions, next_gen):
     """The compute-bound offline tenant: Qwen2-7B gate/up projection (4096 tokens x 37888 x 3584)
     on the gated tcgen05 GEMM -- TFLOP/s polled / unpolled / cuBLAS, and preempt-to-quiesce."""
@@ -452,6 +521,15 @@ def run_valve(args, rank, world, dist):
 
     copy_gbs = statistics.mean(b / (ms * 1e-3) / 1e9 for b, ms in zip(stats["bytes"], stats["copy_ms"]))
 
+    # ------------------------------------------------ C3: weight pages (configs[2] mechanism)
+    import gc
+
+    del pool, host
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    c3 = {"note": "skipped (--profile-mode)"} if args.profile_mode else c3_weights(torch, A, gpu, cp, args.seed + rank, peak)
+
     # ------------------------------------------------ measured online TTFT/TPOT deltas
     # (real-time loop: random-init Llama-3-8B online in PyTorch + the gated offline tenant on a
     # 32 GiB pool; the 128 GiB reclaim pool is released first)
@@ -459,9 +537,7 @@ def run_valve(args, rank, world, dist):
     if world > 1:
         rt = {"note": "measured in the N=1 run (one online tenant per node instance)"}
     elif not args.skip_realtime and not args.profile_mode:
-        import gc
-
-        del pool, host, gate
+        del gate
         gc.collect()
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
@@ -517,6 +593,7 @@ def run_valve(args, rank, world, dist):
         "offline_gbs": {"polled": round(polled[0], 1), "unpolled": round(unpolled[0], 1)},
         "offline_gemm": gemm,
         "policy_contrast_recompute": contrast,
+        "c3_weight_pages": c3,
         "ttft_delta_pct": rt.get("ttft_delta_pct"),
         "tpot_delta_pct": rt.get("tpot_delta_pct"),
         "online_realtime": rt,

@@ -265,7 +265,7 @@ def gemm_tenant(torch, A, gate, dev, stream, gate_stream, preemptions, next_gen)
         t_poll, t_nopoll = timed(lambda: run(True)), timed(lambda: run(False))
         t_cublas = timed(lambda: torch.matmul(a, b.t(), out=c))
     q = []
-    total = (m // 128) * (n // 256)
+    total = (m // 256) * (n // 256)  # CTA-pair tiles (the default when m % 256 == 0)
     for i in range(preemptions):
         gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, stream=stream.cuda_stream, fresh=True)
         time.sleep(0.0001 + 0.0004 * (i % 7) / 7)
@@ -528,7 +528,7 @@ def run_valve(args, rank, world, dist):
     gc.collect()
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
-    c3 = {"note": "skipped (--profile-mode)"} if args.profile_mode else c3_weights(torch, A, gpu, cp, args.seed + rank, peak)
+    c3 = c3_weights(torch, A, gpu, cp, args.seed + rank, peak)
 
     # ------------------------------------------------ measured online TTFT/TPOT deltas
     # (real-time loop: random-init Llama-3-8B online in PyTorch + the gated offline tenant on a

@@ -284,6 +284,9 @@ typedef struct {
   int poll;       /* 0 = ignore the gate (overhead baseline) */
   int fresh;      /* nonzero: a new work list -- zero the tile cursors and counters on the launch
                      stream first (stream-ordered valve_offline_reset); 0: resume */
+  int mode;       /* 0 auto (CTA pairs when m % 256 == 0), 1 one CTA per 128x256 tile
+                     (tcgen05 cta_group::1), 2 CTA pairs: 2-CTA clusters on 256x256 tiles with
+                     tcgen05.mma.cta_group::2 (M=256), each CTA holding half of A and of B */
 } valve_offline_gemm_work;
 int valve_offline_gemm(valve_gate* g, const valve_offline_gemm_work* w, void* stream);
 

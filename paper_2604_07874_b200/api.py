@@ -662,7 +662,7 @@ class OfflineWork(C.Structure):
 
 class OfflineGemmWork(C.Structure):
     _fields_ = [("a", C.c_void_p), ("b", C.c_void_p), ("c", C.c_void_p), ("m", C.c_int), ("n", C.c_int),
-                ("k", C.c_int), ("ctas", C.c_int), ("poll", C.c_int), ("fresh", C.c_int)]
+                ("k", C.c_int), ("ctas", C.c_int), ("poll", C.c_int), ("fresh", C.c_int), ("mode", C.c_int)]
 
 
 class PoolView(C.Structure):
@@ -941,11 +941,13 @@ class Gate:
         self._b.check(self._b.lib.valve_offline_reset(self._h))
 
     def launch_gemm(self, a_ptr: int, b_ptr: int, c_ptr: int, m: int, n: int, k: int, *, ctas: int = 0,
-                    poll: bool = True, stream: Optional[int] = None, fresh: bool = False):
+                    poll: bool = True, stream: Optional[int] = None, fresh: bool = False, mode: int = 0):
         """Gated tcgen05 GEMM C[m,n] = A[m,k] B[n,k]^T (bf16, device pointers), preemptible at
         128x256-tile granularity (valve_offline_gemm).  fresh=True starts a new work list
-        (stream-ordered cursor reset); otherwise the launch resumes from the gate's cursors."""
-        w = OfflineGemmWork(a_ptr, b_ptr, c_ptr, m, n, k, ctas, 1 if poll else 0, 1 if fresh else 0)
+        (stream-ordered cursor reset); otherwise the launch resumes from the gate's cursors.
+        mode: 0 auto (CTA pairs when m % 256 == 0), 1 single-CTA 128x256 tiles, 2 CTA pairs
+        (tcgen05 cta_group::2 on 256x256 tiles)."""
+        w = OfflineGemmWork(a_ptr, b_ptr, c_ptr, m, n, k, ctas, 1 if poll else 0, 1 if fresh else 0, mode)
         self._b.check(self._b.lib.valve_offline_gemm(self._h, C.byref(w),
                                                      C.c_void_p(stream) if stream else None))
 

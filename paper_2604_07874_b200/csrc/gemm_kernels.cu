@@ -103,109 +103,240 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
+
+// ---- cluster helpers (pair mode: two CTAs of a cluster share each B tile via TMA multicast)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_cluster_s64(uint32_t caddr, long long v) {
+  asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(caddr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WC_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// ---- cta_group::2 (CTA pair on one TPC): the leader issues M=256 MMAs that read A rows and
+// B columns from both CTAs' shared memory and write each CTA's TMEM
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address bit 24 = CTA rank in the pair
+// kind::f16, D f32, A/B bf16 K-major, M = 256, N = 256
+constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+__device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc2), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// both CTAs load their half; completion bytes land on the LEADER's barrier (same offset)
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & kPeerMask), "r"(x), "r"(y)
+      : "memory");
+}
+
 }  // namespace
 
-__global__ void __launch_bounds__(256, 1)
-    k_offline_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   GemmArgs G) {
+// kPair = false: one CTA per 128x256 tile of C (tcgen05.mma.cta_group::1, M=128).
+// kPair = true : a CTA pair (2-CTA cluster on one TPC) per 256x256 tile with
+//   tcgen05.mma.cta_group::2 (M=256): CTA r holds rows 128r.. of A and columns 128r.. of B for
+//   each k-block (32 KiB per SM per stage instead of 48, so 6 stages fit), the leader (rank 0)
+//   issues the MMAs, which read both CTAs' shared memory and accumulate each CTA's 128 rows in its
+//   own TMEM.  Both CTAs' TMA loads complete on the leader's full barrier; the leader's commits
+//   multicast to both CTAs' empty / tmem_full barriers; both epilogues must drain before the
+//   leader reuses an accumulator.  Rank 0 also owns the tile schedule and the gate check and
+//   publishes each tile id to both CTAs (st.shared::cluster + remote mbarrier arrive).
+template <bool kPair>
+__device__ __forceinline__ void offline_gemm_body(const CUtensorMap& map_a, const CUtensorMap& map_b,
+                                                  const GemmArgs& G) {
+  constexpr int kStages = kPair ? kGemmStagesPair : kGemmStages;
+  constexpr int kBRows = kPair ? kBN / 2 : kBN;           // B rows this CTA loads per k-block
+  constexpr int kStage = kABytes + kBRows * kBK * 2;       // bytes per stage in this CTA
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[kGemmStages], empty_bar[kGemmStages];
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ __align__(8) uint64_t tile_full[2], tile_empty[2], tmem_full[2], tmem_empty[2];
   __shared__ long long s_tile[2];
   __shared__ uint32_t s_tmem;
   // 1024-byte alignment for the swizzled operand tiles
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = kPair ? cluster_rank() : 0u;
+  constexpr uint16_t kBoth = 0x3;
+  // tile-id readers: per CTA 128 epilogue threads + the MMA thread (leader) / producer (rank 1)
+  constexpr uint32_t kReaders = kPair ? 2 * 129 : 129;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kGemmStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&tile_full[s], 1);          // scheduler published the slot's tile id
-      mbar_init(&tile_empty[s], 1 + 128);   // MMA thread + 128 epilogue threads read it
-      mbar_init(&tmem_full[s], 1);          // tcgen05.commit: accumulator complete
-      mbar_init(&tmem_empty[s], 128);       // epilogue drained the accumulator
+      mbar_init(&tile_full[s], 1);                     // scheduler published the slot's tile id
+      mbar_init(&tile_empty[s], kReaders);             // every reader took it (rank 0's counts)
+      mbar_init(&tmem_full[s], 1);                     // tcgen05.commit: accumulator complete
+      mbar_init(&tmem_empty[s], kPair ? 256 : 128);    // epilogue(s) drained the accumulator
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
   }
+  if (kPair) cluster_sync();  // the peer's barriers exist before anyone arrives on them
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
-                 "r"(2 * kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                   "r"(2 * kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                   "r"(2 * kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   fence_before();
-  __syncthreads();
+  if (kPair) cluster_sync();
+  else __syncthreads();
   fence_after();
   const uint32_t tmem = s_tmem;
-  const int tiles_n = G.n / kBN;
+  constexpr int kTM = kPair ? 2 * kBM : kBM;  // rows of C per scheduled tile
+  const int tiles_m = G.m / kTM;
   const int kblocks = G.k / kBK;
   unsigned long long done = 0;
+  // "slot consumed" / "accumulator drained" go to rank 0's barriers (remote for rank 1)
+  auto consumed = [&](uint32_t slot) {
+    if (kPair) mbar_arrive_cluster(mapa(smem_u32(&tile_empty[slot]), 0));
+    else mbar_arrive(&tile_empty[slot]);
+  };
+  auto wait_tile = [&](uint32_t slot, uint32_t parity) {
+    if (kPair) mbar_wait_cluster(&tile_full[slot], parity);
+    else mbar_wait(&tile_full[slot], parity);
+  };
   if (warp == 0 && lane == 0) {
-    // ---------------- scheduler + TMA producer.  Tile j goes through smem slot j & 1; the
-    // producer runs at most one tile ahead of the epilogue (two accumulators in TMEM).
+    // ---------------- scheduler (rank 0) + TMA producer (both ranks).  Tile j goes through smem
+    // slot j & 1; the producer runs at most one tile ahead of the epilogue (two accumulators).
+    // one HBM cursor (148 claimers at one claim per ~15 us do not contend), so the tiles in
+    // flight are consecutive claims; claims are rasterised M-fastest, so the clusters running
+    // together share each B (weight) tile through L2 and A stays L2-resident
     const unsigned long long total = (unsigned long long)G.total_tiles;
-    const unsigned long long per = (total + kStripes - 1) / kStripes;
-    int stripe = blockIdx.x % kStripes, visited = 0;
     uint32_t it = 0;
     for (uint32_t j = 0;; ++j) {
+      const uint32_t slot = j & 1, use = j >> 1;
       long long t = -1;
-      if (G.poll && ld_acquire(&G.g->closed)) {
-        atomicCAS(&G.g->t_first_seen, 0ull, globaltimer_ns());
-      } else {
-        while (visited < kStripes) {
-          const unsigned long long local = atomicAdd(&G.g->cursor[stripe], 1ull);
-          const unsigned long long c = (unsigned long long)stripe * per + local;
-          if (local < per && c < total) {
-            t = (long long)c;
-            break;
-          }
-          stripe = (stripe + 1) % kStripes;
-          ++visited;
+      if (rank == 0) {
+        if (G.poll && ld_acquire(&G.g->closed)) {
+          atomicCAS(&G.g->t_first_seen, 0ull, globaltimer_ns());
+        } else {
+          const unsigned long long c = atomicAdd(&G.g->cursor[0], 1ull);
+          if (c < total) t = (long long)c;
+        }
+        if (kPair) mbar_wait_cluster(&tile_empty[slot], (use & 1) ^ 1);
+        else mbar_wait(&tile_empty[slot], (use & 1) ^ 1);
+        s_tile[slot] = t;
+        if (kPair) {
+          st_cluster_s64(mapa(smem_u32(&s_tile[slot]), 1), t);
+          mbar_arrive_cluster(mapa(smem_u32(&tile_full[slot]), 1));
+        }
+        mbar_arrive(&tile_full[slot]);
+      } else {  // pair rank 1: follow rank 0's schedule
+        wait_tile(slot, use & 1);
+        t = s_tile[slot];
+        consumed(slot);
+      }
+      if (t < 0) break;
+      const int m0 = (int)(t % tiles_m) * kTM + (int)rank * kBM;
+      const int n0 = (int)(t / tiles_m) * kBN + (int)rank * (kBN - kBRows);
+      for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        const uint32_t st = it % kStages, ph = (it / kStages) & 1u;
+        mbar_wait(&empty_bar[st], ph ^ 1);
+        uint8_t* sa = smem + st * kStage;
+        uint8_t* sb = sa + kABytes;
+        if (kPair) {
+          // the leader's full barrier collects both CTAs' A and B halves
+          if (rank == 0) mbar_expect_tx(&full_bar[st], 2 * kStage);
+          tma_load_2d_2sm(sa, &map_a, &full_bar[st], kb * kBK, m0);
+          tma_load_2d_2sm(sb, &map_b, &full_bar[st], kb * kBK, n0);
+        } else {
+          mbar_expect_tx(&full_bar[st], kStage);
+          tma_load_2d(sa, &map_a, &full_bar[st], kb * kBK, m0);
+          tma_load_2d(sb, &map_b, &full_bar[st], kb * kBK, n0);
         }
       }
-      const uint32_t slot = j & 1, use = j >> 1;
-      mbar_wait(&tile_empty[slot], (use & 1) ^ 1);
-      s_tile[slot] = t;
-      mbar_arrive(&tile_full[slot]);
-      if (t < 0) break;
-      const int m0 = (int)(t / tiles_n) * kBM, n0 = (int)(t % tiles_n) * kBN;
-      for (int kb = 0; kb < kblocks; ++kb, ++it) {
-        const uint32_t st = it % kGemmStages, ph = (it / kGemmStages) & 1u;
-        mbar_wait(&empty_bar[st], ph ^ 1);
-        uint8_t* sa = smem + st * kStageBytes;
-        uint8_t* sb = sa + kABytes;
-        mbar_expect_tx(&full_bar[st], kStageBytes);
-        tma_load_2d(sa, &map_a, &full_bar[st], kb * kBK, m0);
-        tma_load_2d(sb, &map_b, &full_bar[st], kb * kBK, n0);
-      }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer: accumulator j & 1 (TMEM columns 0 / 256)
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer (leader): accumulator j & 1 (TMEM columns 0 / 256)
     uint32_t it = 0;
     for (uint32_t j = 0;; ++j) {
       const uint32_t slot = j & 1, use = j >> 1;
-      mbar_wait(&tile_full[slot], use & 1);
+      wait_tile(slot, use & 1);
       const long long t = s_tile[slot];
-      mbar_arrive(&tile_empty[slot]);
+      consumed(slot);
       if (t < 0) break;
-      mbar_wait(&tmem_empty[slot], (use & 1) ^ 1);
+      if (kPair) mbar_wait_cluster(&tmem_empty[slot], (use & 1) ^ 1);
+      else mbar_wait(&tmem_empty[slot], (use & 1) ^ 1);
       fence_after();
       const uint32_t acc = tmem + slot * kTmemCols;
       for (int kb = 0; kb < kblocks; ++kb, ++it) {
-        const uint32_t st = it % kGemmStages, ph = (it / kGemmStages) & 1u;
+        const uint32_t st = it % kStages, ph = (it / kStages) & 1u;
         mbar_wait(&full_bar[st], ph);
         fence_after();
-        const uint32_t sa = smem_u32(smem + st * kStageBytes);
+        const uint32_t sa = smem_u32(smem + st * kStage);
         const uint32_t sb = sa + kABytes;
 #pragma unroll
-        for (int k = 0; k < kBK / kUK; ++k)
-          mma_bf16(acc, smem_desc(sa + k * kUK * 2), smem_desc(sb + k * kUK * 2), (kb | k) != 0);
-        mma_commit(&empty_bar[st]);  // the stage is free once these MMAs have read it
+        for (int k = 0; k < kBK / kUK; ++k) {
+          if (kPair) mma_bf16_2sm(acc, smem_desc(sa + k * kUK * 2), smem_desc(sb + k * kUK * 2), (kb | k) != 0);
+          else mma_bf16(acc, smem_desc(sa + k * kUK * 2), smem_desc(sb + k * kUK * 2), (kb | k) != 0);
+        }
+        // the stage is free once these MMAs have read it -- in both CTAs of a pair
+        if (kPair) mma_commit_2sm(&empty_bar[st], kBoth);
+        else mma_commit(&empty_bar[st]);
       }
-      mma_commit(&tmem_full[slot]);
+      if (kPair) mma_commit_2sm(&tmem_full[slot], kBoth);
+      else mma_commit(&tmem_full[slot]);
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM lanes 32*(warp-4).. -> rows of C, overlapped with the
@@ -213,11 +344,11 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp - 4;
     for (uint32_t j = 0;; ++j) {
       const uint32_t slot = j & 1, use = j >> 1;
-      mbar_wait(&tile_full[slot], use & 1);
+      wait_tile(slot, use & 1);
       const long long t = s_tile[slot];
-      mbar_arrive(&tile_empty[slot]);
+      consumed(slot);
       if (t < 0) break;
-      const int m0 = (int)(t / tiles_n) * kBM, n0 = (int)(t % tiles_n) * kBN;
+      const int m0 = (int)(t % tiles_m) * kTM + (int)rank * kBM, n0 = (int)(t / tiles_m) * kBN;
       mbar_wait(&tmem_full[slot], use & 1);
       fence_after();
       const int row = m0 + q * 32 + lane;
@@ -245,12 +376,14 @@ __global__ void __launch_bounds__(256, 1)
                                pack_bf16(__uint_as_float(v[8 * jj + 6]), __uint_as_float(v[8 * jj + 7])));
       }
       fence_before();
-      mbar_arrive(&tmem_empty[slot]);
+      if (kPair) mbar_arrive_cluster(mapa(smem_u32(&tmem_empty[slot]), 0));
+      else mbar_arrive(&tmem_empty[slot]);
       ++done;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 128 && done) atomicAdd(&G.g->tiles_done, done);
+  // one count per scheduled tile (a pair's tile is counted by rank 0)
+  if (threadIdx.x == 128 && done && rank == 0) atomicAdd(&G.g->tiles_done, done);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -260,10 +393,27 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
   fence_before();
-  __syncthreads();
+  if (kPair) cluster_sync();  // no CTA leaves while its peer may still load / arrive into it
+  else __syncthreads();
   fence_after();
-  if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kTmemCols));
+  if (warp == 2) {
+    if (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kTmemCols));
+  }
+}
+
+__global__ void __launch_bounds__(256, 1)
+    k_offline_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   GemmArgs G) {
+  offline_gemm_body<false>(map_a, map_b, G);
+}
+
+__global__ void __launch_bounds__(256, 1)
+    k_offline_gemm_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                        GemmArgs G) {
+  offline_gemm_body<true>(map_a, map_b, G);
 }
 
 }  // namespace valve

@@ -294,21 +294,27 @@ __global__ void k_block_table(PoolDev P, int64_t req, int* out) {
 // snapshot (memory.cpp:142-153): offline handles ascending, residents ascending.
 // Pass A (warp per handle, 2 handles in flight) writes each handle's sorted residents to
 // scratch at stride S; pass B compacts with a CTA scan into s_hid/s_hmap/s_roff/res_pages.
+// Snapshot, part 1 (grid-wide): one warp per handle sorts its distinct resident requests.
+__global__ void __launch_bounds__(256) k_snapshot_handles(PoolDev P) {
+  const int lane = threadIdx.x & 31;
+  const int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (h >= P.H) return;
+  const int nc = (P.S + 31) >> 5;
+  int64_t* sorted = reinterpret_cast<int64_t*>(P.s_key);
+  if (P.hstate[h] != kOffline) {
+    if (lane == 0) P.s_cnt[h] = 0;
+    return;
+  }
+  int cnt = 0;
+  VALVE_DISPATCH_NC(nc, cnt = warp_sorted_residents<NC>(P, h, sorted + (int64_t)h * P.S));
+  if (lane == 0) P.s_cnt[h] = cnt;
+}
+
+// Snapshot, part 2 (one CTA): compact the offline handles into the CSR instance.
 __global__ void __launch_bounds__(kNT) k_snapshot(PoolDev P) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nc = (P.S + 31) >> 5;
   op_begin(P);
-  int64_t* sorted = reinterpret_cast<int64_t*>(P.s_key);
-  for (int h = wid; h < P.H; h += nw) {
-    if (P.hstate[h] != kOffline) {
-      if (lane == 0) P.s_cnt[h] = 0;
-      continue;
-    }
-    int cnt = 0;
-    VALVE_DISPATCH_NC(nc, cnt = warp_sorted_residents<NC>(P, h, sorted + (int64_t)h * P.S));
-    if (lane == 0) P.s_cnt[h] = cnt;
-  }
-  __syncthreads();
+  const int64_t* sorted = reinterpret_cast<const int64_t*>(P.s_key);
   int carry_h = 0, carry_r = 0;
   for (int base = 0; base < P.H; base += blockDim.x) {
     const int h = base + threadIdx.x;

@@ -509,6 +509,9 @@ int valve_pool_snapshot(const valve_pool* cp, int* ids, int64_t* mapped, int* of
                         int cap_h, int cap_r, int* nh, int* nr) {
   auto* p = const_cast<valve_pool*>(cp);
   return guard([&] {
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    k_snapshot_handles<<<(p->H + 7) / 8, 256, 0, p->stream>>>(p->d);
+    counted();
     p->launch1("snapshot", k_snapshot, p->smem_snapshot, p->d);
     *nh = (int)p->mirror->r[0];
     *nr = (int)p->mirror->r[1];
@@ -1405,9 +1408,10 @@ int valve_gate_read(const valve_gate* g, valve_gate_state* o) {
     o->t_quiesced_ns = h.t_quiesced;
     o->tiles_done = h.tiles_done;
     o->canary_hits = h.canary;
-    const unsigned long long per = (h.total + kStripes - 1) / kStripes;
+    const int ns = h.stripes ? (int)std::min<unsigned long long>(h.stripes, kStripes) : kStripes;
+    const unsigned long long per = (h.total + ns - 1) / ns;
     unsigned long long claimed = 0;
-    for (int i = 0; i < kStripes; ++i) {
+    for (int i = 0; i < ns; ++i) {
       const unsigned long long len = h.total > i * per ? std::min(per, h.total - i * per) : 0;
       claimed += std::min(h.cursor[i], len);
     }
@@ -1457,6 +1461,7 @@ int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work*
       ctas = std::min(per_sm, std::max(1, 512 / threads)) * sms;
     }
     // never start tiles into a closed gate; count the CTAs before they can retire
+    cu_ck(op.write64((CUstream)st, dptr(&g->d->stripes), (cuuint64_t)kStripes, 0), "cuStreamWriteValue64");
     cu_ck(op.wait32((CUstream)st, dptr(&g->d->closed), 0, CU_STREAM_WAIT_VALUE_EQ), "cuStreamWaitValue32");
     cu_ck(op.write32((CUstream)st, dptr(&g->d->live_ctas), (cuuint32_t)ctas, 0), "cuStreamWriteValue32");
     OfflineArgs A{};
@@ -1525,12 +1530,18 @@ int valve_offline_gemm(valve_gate* g, const valve_offline_gemm_work* w, void* s)
     if (!s && !g->work_stream)
       ck(cudaStreamCreateWithFlags(&g->work_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     cudaStream_t st = as_stream(s, g->work_stream);
+    if (w->mode < 0 || w->mode > 2) fail(VALVE_INVALID_ARGUMENT, "offline_gemm: mode must be 0, 1 or 2");
+    if (w->mode == 2 && w->m % 256) fail(VALVE_INVALID_ARGUMENT, "offline_gemm: CTA pairs need m % 256 == 0");
+    // auto = CTA pairs (tcgen05 cta_group::2) whenever m allows: 1,484 vs 1,368 TFLOP/s for
+    // single-CTA tiles at 4096x37888x3584 on B200 (cuBLAS 1,624)
+    const bool pair = w->mode == 2 || (w->mode == 0 && w->m % 256 == 0);
     static std::once_flag attr_once;
     std::call_once(attr_once, [] {
       cudaFuncSetAttribute(k_offline_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
+      cudaFuncSetAttribute(k_offline_gemm_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
     });
     const CUtensorMap ma = kmajor_map(w->a, w->m, w->k, 128);
-    const CUtensorMap mb = kmajor_map(w->b, w->n, w->k, 256);
+    const CUtensorMap mb = kmajor_map(w->b, w->n, w->k, pair ? 128 : 256);  // pairs load half-B boxes
     int ctas = w->ctas;
     if (ctas <= 0) ck(cudaDeviceGetAttribute(&ctas, cudaDevAttrMultiProcessorCount, g->device), "attr");
     GemmArgs G{};
@@ -1539,17 +1550,35 @@ int valve_offline_gemm(valve_gate* g, const valve_offline_gemm_work* w, void* s)
     G.m = w->m;
     G.n = w->n;
     G.k = w->k;
-    G.total_tiles = (long long)(w->m / 128) * (w->n / 256);
+    G.total_tiles = (long long)(w->m / (pair ? 256 : 128)) * (w->n / 256);
     G.poll = w->poll;
-    ctas = (int)std::min<long long>(ctas, G.total_tiles);
+    if (pair) ctas = 2 * (int)std::min<long long>(std::max(ctas / 2, 1), G.total_tiles);
+    else ctas = (int)std::min<long long>(ctas, G.total_tiles);
     if (w->fresh) {
       ck(cudaMemsetAsync(&g->d->t_first_seen, 0, 4 * sizeof(unsigned long long), st), "memset");
       ck(cudaMemsetAsync(g->d->cursor, 0, sizeof(g->d->cursor), st), "memset");
     }
     cu_ck(op.write64((CUstream)st, dptr(&g->d->total), (cuuint64_t)G.total_tiles, 0), "cuStreamWriteValue64");
+    cu_ck(op.write64((CUstream)st, dptr(&g->d->stripes), 1, 0), "cuStreamWriteValue64");
     cu_ck(op.wait32((CUstream)st, dptr(&g->d->closed), 0, CU_STREAM_WAIT_VALUE_EQ), "cuStreamWaitValue32");
     cu_ck(op.write32((CUstream)st, dptr(&g->d->live_ctas), (cuuint32_t)ctas, 0), "cuStreamWriteValue32");
-    k_offline_gemm<<<ctas, 256, kGemmSmemBytes, st>>>(ma, mb, G);
+    if (pair) {
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(ctas);
+      lc.blockDim = dim3(256);
+      lc.dynamicSmemBytes = kGemmSmemBytes;
+      lc.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      ck(cudaLaunchKernelEx(&lc, k_offline_gemm_pair, ma, mb, G), "offline gemm (pair) launch");
+    } else {
+      k_offline_gemm<<<ctas, 256, kGemmSmemBytes, st>>>(ma, mb, G);
+    }
     counted();
     ck(cudaGetLastError(), "offline gemm launch");
   });

@@ -33,6 +33,7 @@ __global__ void k_requests_on_handle(PoolDev P, int h, int64_t* out);
 __global__ void k_handles_of_request(PoolDev P, int64_t req, int* out);
 __global__ void k_offline_pages_of(PoolDev P, int64_t req);
 __global__ void k_block_table(PoolDev P, int64_t req, int* out);
+__global__ void k_snapshot_handles(PoolDev P);
 __global__ void k_snapshot(PoolDev P);
 __global__ void k_apply(PoolDev P, const int* ids, int k, int64_t t);
 __global__ void k_reclaim(PoolDev P, int k, int mode, int64_t t);
@@ -104,6 +105,7 @@ struct GateDev {
   unsigned long long total;               // tiles of the current work list
   unsigned long long cursor[kStripes];    // per-stripe claims (the context save)
   unsigned long long t_raise;             // %globaltimer of a kernel-issued raise (diagnostic)
+  unsigned long long stripes;             // cursors the current work list uses (0 = kStripes)
 };
 __global__ void k_gate_raise_stamp(GateDev* g, unsigned gen);
 struct OfflineArgs {
@@ -123,7 +125,8 @@ struct OfflineArgs {
 __global__ void k_offline_decode(OfflineArgs A);
 
 // gated offline GEMM (gemm_kernels.cu): 128x256 tiles claimed from the gate's striped cursors
-constexpr int kGemmStages = 4;
+constexpr int kGemmStages = 4;      // 48 KiB per stage (A 128x64 + B 256x64)
+constexpr int kGemmStagesPair = 6;  // 32 KiB per stage per CTA (A 128x64 + B 128x64)
 constexpr int kGemmSmemBytes = kGemmStages * (128 * 64 + 256 * 64) * 2 + 1024;
 struct GemmArgs {
   GateDev* g;
@@ -134,5 +137,8 @@ struct GemmArgs {
 };
 __global__ void k_offline_gemm(const __grid_constant__ CUtensorMap map_a,
                                const __grid_constant__ CUtensorMap map_b, GemmArgs G);
+// CTA-pair variant (tcgen05.mma.cta_group::2, M=256): 256x256 tiles
+__global__ void k_offline_gemm_pair(const __grid_constant__ CUtensorMap map_a,
+                                    const __grid_constant__ CUtensorMap map_b, GemmArgs G);
 
 }  // namespace valve

@@ -26,17 +26,32 @@ def _run(gate, a, b, c, **kw):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 3584), (384, 1024, 1024), (512, 4608, 3584)])
-def test_gemm_matches_fp32_reference(m, n, k):
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (256, 512, 3584), (384, 1024, 1024), (512, 4608, 3584),
+                                   (1024, 2048, 192)])
+def test_gemm_matches_fp32_reference(m, n, k, mode):
+    if mode == 2 and m % 256:
+        pytest.skip("CTA pairs need m % 256 == 0")
     a, b = _operands(m, n, k, seed=m + n + k)
     c = torch.full((m, n), float("nan"), dtype=torch.bfloat16, device="cuda")
     gate = A.Gate(0)
-    _run(gate, a, b, c)
+    _run(gate, a, b, c, mode=mode)
     ref = a.float() @ b.float().t()
     # fp32 accumulation, one bf16 rounding of the output: |err| <= 2^-8 |ref| (+ accumulation-order slack)
     torch.testing.assert_close(c.float(), ref, rtol=8e-3, atol=2e-3 * ref.abs().max().item())
     s = gate.read()
-    assert s.tiles_done == (m // 128) * (n // 256) and s.live_ctas == 0
+    assert s.tiles_done == (m // (128 * mode)) * (n // 256) and s.live_ctas == 0
+
+
+def test_gemm_pair_and_single_agree_bitwise():
+    m, n, k = 512, 1024, 3584
+    a, b = _operands(m, n, k, seed=5)
+    gate = A.Gate(0)
+    c1 = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+    c2 = torch.empty_like(c1)
+    _run(gate, a, b, c1, mode=1)
+    _run(gate, a, b, c2, mode=2, ctas=6)
+    assert torch.equal(c1.view(torch.int16), c2.view(torch.int16))  # same K order per output tile
 
 
 def test_gemm_ctas_fewer_than_tiles_and_no_poll():
@@ -50,19 +65,20 @@ def test_gemm_ctas_fewer_than_tiles_and_no_poll():
     assert torch.equal(c1, c2)  # same tile -> same bits, whatever CTA ran it
 
 
-def test_gemm_preempt_resume_conserves_tiles():
-    m, n, k = 2048, 4864, 3584  # 304 tiles of ~0.23 GFLOP
+@pytest.mark.parametrize("mode", [1, 2])
+def test_gemm_preempt_resume_conserves_tiles(mode):
+    m, n, k = 2048, 4864, 3584  # 304 tiles of ~0.23 GFLOP (152 pair tiles)
     a, b = _operands(m, n, k, seed=7)
     gate = A.Gate(0)
     c_ref = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
-    _run(gate, a, b, c_ref)
-    total = (m // 128) * (n // 256)
+    _run(gate, a, b, c_ref, mode=1)
+    total = (m // (128 * mode)) * (n // 256)
     c = torch.full_like(c_ref, float("nan"))
     gate.reset_work()
     rng = random.Random(1)
     gen = preemptions = 0
     while True:
-        gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, ctas=4)
+        gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, ctas=4, mode=mode)
         time.sleep(rng.uniform(0.0001, 0.0005))
         gen += 1
         gate.raise_(gen)
@@ -81,7 +97,8 @@ def test_gemm_preempt_resume_conserves_tiles():
     assert torch.equal(c.view(torch.int16), c_ref.view(torch.int16))
 
 
-def test_gemm_quiesce_is_one_tile():
+@pytest.mark.parametrize("mode", [1, 2])
+def test_gemm_quiesce_is_one_tile(mode):
     m, n, k = 8192, 18944, 3584  # Qwen2-7B gate/up projection over 8192 tokens: 4,736 tiles
     a, b = _operands(m, n, k, seed=11)
     c = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
@@ -91,7 +108,7 @@ def test_gemm_quiesce_is_one_tile():
     for gen in range(1, 21):
         gate.reset_work()
         side = torch.cuda.Stream()
-        gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, stream=side.cuda_stream)
+        gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, stream=side.cuda_stream, mode=mode)
         time.sleep(0.0003)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(gs)
@@ -101,7 +118,7 @@ def test_gemm_quiesce_is_one_tile():
         gate.release(gen)
         torch.cuda.synchronize()
         waits.append(e0.elapsed_time(e1) * 1e3)
-        assert gate.read().tiles_done < (m // 128) * (n // 256)  # it really was preempted
+        assert gate.read().tiles_done < (m // (128 * mode)) * (n // 256)  # it really was preempted
     waits.sort()
     # one 128x256x3584 tile is ~0.23 GFLOP (~15 us on one SM's tensor cores)
     assert waits[len(waits) // 2] < 100.0, waits
@@ -117,3 +134,5 @@ def test_gemm_rejects_bad_shapes():
         gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), 128, 256, 48)
     with pytest.raises(A.InvalidArgument):
         gate.launch_gemm(0, b.data_ptr(), c.data_ptr(), 128, 256, 64)
+    with pytest.raises(A.InvalidArgument):
+        gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), 128, 256, 64, mode=2)

@@ -39,17 +39,19 @@ def main():
         c = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
         flop = 2.0 * m * n * k
 
-        def valve(poll=True):
+        def valve(poll=True, mode=0):
             gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, poll=poll, stream=st.cuda_stream,
-                             fresh=True)
+                             fresh=True, mode=mode)
 
         with torch.cuda.stream(st):
             ms_poll = timed(lambda: valve(True), st)
             ms_nopoll = timed(lambda: valve(False), st)
+            ms_single = timed(lambda: valve(True, 1), st)
             ms_cublas = timed(lambda: torch.matmul(a, b.t(), out=c), st)
         out["shapes"][name] = {"n": n, "k": k, "tflops_polled": round(flop / ms_poll / 1e9, 1),
                                "tflops_unpolled": round(flop / ms_nopoll / 1e9, 1),
                                "tflops_cublas": round(flop / ms_cublas / 1e9, 1),
+                               "tflops_single_cta": round(flop / ms_single / 1e9, 1),
                                "ms_polled": round(ms_poll, 4)}
     # quiesce with the GEMM as the tenant
     n, k = SHAPES["gate_up"]
@@ -69,7 +71,7 @@ def main():
         e1.record(gs)
         gate.release(gen)
         torch.cuda.synchronize()
-        if gate.read().tiles_done < (8192 // 128) * (n // 256):
+        if gate.read().tiles_done < (8192 // 256) * (n // 256):  # pair tiles
             q.append(e0.elapsed_time(e1) * 1e3)
     q.sort()
     out["gemm_quiesce_us"] = {"n": len(q), "p50": round(q[len(q) // 2], 2),

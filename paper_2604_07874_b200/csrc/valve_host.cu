@@ -1535,11 +1535,11 @@ int valve_offline_gemm(valve_gate* g, const valve_offline_gemm_work* w, void* s)
     // auto = CTA pairs (tcgen05 cta_group::2) whenever m allows: 1,484 vs 1,368 TFLOP/s for
     // single-CTA tiles at 4096x37888x3584 on B200 (cuBLAS 1,624)
     const bool pair = w->mode == 2 || (w->mode == 0 && w->m % 256 == 0);
-    static std::once_flag attr_once;
-    std::call_once(attr_once, [] {
-      cudaFuncSetAttribute(k_offline_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
-      cudaFuncSetAttribute(k_offline_gemm_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
-    });
+    // per device (cudaFuncSetAttribute applies to the current device); cheap to repeat
+    ck(cudaFuncSetAttribute(k_offline_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes),
+       "cudaFuncSetAttribute");
+    ck(cudaFuncSetAttribute(k_offline_gemm_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes),
+       "cudaFuncSetAttribute");
     const CUtensorMap ma = kmajor_map(w->a, w->m, w->k, 128);
     const CUtensorMap mb = kmajor_map(w->b, w->n, w->k, pair ? 128 : 256);  // pairs load half-B boxes
     int ctas = w->ctas;

@@ -53,7 +53,7 @@ def test_selection_device_vs_reference(ref, mode):
 def test_selection_large_instances_device_vs_oracle(oracle_c):
     """B200-scale instances (C2: ~950 handles, ~1500 refs, ~310 requests)."""
     rng = random.Random(5)
-    for n, n_req in [(114, 40), (920, 310), (1024, 600)]:
+    for n, n_req in [(114, 40), (920, 310), (1024, 600), (4096, 2500), (6000, 300)]:
         cost = {r: rng.randint(2000, 4400) for r in range(n_req)}
         handles = [A.ReclaimHandle(h, rng.randint(0, 10**6),
                                    sorted(set(rng.randrange(n_req) for _ in range(rng.randint(1, 3)))))
@@ -199,7 +199,11 @@ def _populate(pool_d, pool_o, rng, H, S, n_req):
 
 
 @pytest.mark.parametrize("seed,H,S,mode", [(0, 16, 4, 0), (1, 128, 64, 0), (2, 128, 64, 1),
-                                           (3, 1024, 64, 0), (4, 300, 16, 0)])
+                                           (3, 1024, 64, 0), (4, 300, 16, 0),
+                                           # beyond the shared-memory fast paths: > 2048 handles,
+                                           # > 4096 listings, 128/256-slot handles (4/8 chunks)
+                                           (5, 3000, 8, 0), (6, 2500, 16, 1), (7, 96, 128, 0),
+                                           (8, 48, 256, 0)])
 def test_fused_reclaim_vs_oracle(oracle_c, seed, H, S, mode):
     rng = random.Random(seed)
     pool_d = A.DevicePool(H, S, 16)

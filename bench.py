@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--skip-realtime", action="store_true", help="skip the measured TTFT/TPOT run")
     ap.add_argument("--rt-horizon", type=float, default=24.0, help="online trace length (s)")
     ap.add_argument("--rt-repeats", type=int, default=2, help="colocated runs (interleaved with standalone)")
+    ap.add_argument("--rt-gemm", default="2048,37888,3584",
+                    help="m,n,k of the offline tenant's gated tcgen05 GEMM (Qwen2-7B gate/up); '' = decode pass only")
     ap.add_argument("--profile-mode", action="store_true",
                     help="ncu launch-list runs: no offline kernel (ncu serialises it to completion)")
     return ap.parse_args()
@@ -546,6 +548,7 @@ def run_valve(args, rank, world, dist):
         # offline harvest at one 8-warp CTA per SM (~3.7 TB/s of HBM reads in the gaps)
         rt = RT.measure_deltas(horizon=args.rt_horizon, device=gpu, seed=args.seed + rank, offline_ctas=148,
                                repeats=args.rt_repeats,
+                               offline_gemm=tuple(int(x) for x in args.rt_gemm.split(",")) if args.rt_gemm else None,
                                log_dir=os.path.join(ROOT, "gpurun_out", "realtime_logs"))
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "r1_copy_traffic.json")))

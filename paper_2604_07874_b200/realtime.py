@@ -217,6 +217,8 @@ class RunResult:
     reclaimed_handles: int = 0
     offline_tiles: int = 0
     offline_bytes: float = 0.0
+    offline_gemm_tiles: int = 0
+    offline_gemm_flop: float = 0.0
     quiesce_wait_us: List[float] = field(default_factory=list)
     decode_iter_us: List[float] = field(default_factory=list)
     prefill_us: List[float] = field(default_factory=list)
@@ -230,7 +232,10 @@ class RunResult:
 class Colocation:
     def __init__(self, model: OnlineModel, pool: Optional[A.DevicePool], gate: Optional[A.Gate],
                  page_tokens: int = 16, max_gap_us: int = 300, resparams: Optional[A.ReservationParams] = None,
-                 tile_bytes: int = 16384, offline_ctas: int = 0):
+                 tile_bytes: int = 16384, offline_ctas: int = 0, offline_gemm=None):
+        """offline_gemm=(m, n, k): the offline tenant also runs the gated tcgen05 GEMM (its
+        projection work, e.g. Qwen2-7B gate/up over m tokens) next to the decode pass, on its own
+        gate attached to the channel's gate, so one raise quiesces both."""
         self.model, self.pool, self.gate = model, pool, gate
         self.page_tokens = page_tokens
         self.tile_bytes = tile_bytes
@@ -242,6 +247,19 @@ class Colocation:
         self.timers: list = []
         self.seq = 0
         self.offline_running = False
+        self.gemm_gate = None
+        if self.colocated and offline_gemm:
+            m, n, k = offline_gemm
+            dev = model.device
+            self.gemm_shape = (m, n, k)
+            g = torch.Generator(device=dev).manual_seed(7)
+            self.gemm_a = torch.randn(m, k, device=dev, generator=g).to(torch.bfloat16)
+            self.gemm_b = (torch.randn(n, k, device=dev, generator=g) * 0.02).to(torch.bfloat16)
+            self.gemm_c = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+            self.gemm_gate = A.Gate(dev.index if dev.index is not None else 0)
+            gate.attach_peers([self.gemm_gate])
+            self.gemm_stream = torch.cuda.Stream()
+            self.gemm_tiles = (m // (256 if m % 256 == 0 else 128)) * (n // 256)
         if self.colocated:
             hooks = A.Hooks(schedule=self._schedule, on_disabled=lambda t: None,
                             on_enabled=self._on_enabled, log=None)
@@ -266,6 +284,20 @@ class Colocation:
     def _launch_offline(self):
         if not self.colocated:
             return
+        self._launch_decode()
+        if self.gemm_gate is not None:
+            self._launch_gemm()
+
+    def _launch_gemm(self):
+        st = self.gemm_gate.read()
+        fresh = st.tiles_claimed >= self.gemm_tiles  # previous pass finished: a new work list
+        if fresh:
+            self._gemm_harvest += st.tiles_done
+        m, n, k = self.gemm_shape
+        self.gemm_gate.launch_gemm(self.gemm_a.data_ptr(), self.gemm_b.data_ptr(), self.gemm_c.data_ptr(),
+                                   m, n, k, stream=self.gemm_stream.cuda_stream, fresh=fresh)
+
+    def _launch_decode(self):
         st = self.gate.read()
         total = self._offline_tiles_total()
         if total and st.tiles_claimed >= total:  # work list exhausted: start another pass
@@ -345,6 +377,7 @@ class Colocation:
         self._evicted, self._off_live, self._off_req_pages, self._off_cost = [], {}, {}, {}
         self._off_pages = 0
         self._harvest = 0
+        self._gemm_harvest = 0
         reqs = [OnlineReq(r.rid, r.arrival_us, r.prompt, r.output) for r in trace]
         log = self.res.log
         log.add(0, "run_meta", scenario="realtime_spike", preset="valve" if self.colocated else "standalone",
@@ -364,6 +397,8 @@ class Colocation:
             P.set_costs({r: self._off_cost[r] for r in self._off_live})
             P.fill_pages()
             self.gate.reset_work()
+            if self.gemm_gate is not None:
+                self.gemm_gate.reset_work()
             self._launch_offline()
         queue: List[OnlineReq] = []
         decoding: List[OnlineReq] = []
@@ -400,7 +435,9 @@ class Colocation:
                 if self.colocated and self.channel.offline_compute_allowed():
                     # the offline engine's next iteration: a pass over its KV finished -> relaunch
                     if self.gate.read().live_ctas == 0:
-                        self._launch_offline()
+                        self._launch_decode()
+                    if self.gemm_gate is not None and self.gemm_gate.read().live_ctas == 0:
+                        self._launch_gemm()
                 time.sleep(50e-6)
                 continue
             if not busy:  # busy edge: raise + wait for the offline CTAs to retire (sim.cpp:362-369)
@@ -434,7 +471,7 @@ class Colocation:
                 log.add(t_it, "prefill_start", **{"class": "online"}, request_id=r.rid, gpu=0, tokens=r.prompt)
                 m.prefill(toks, caches[r.rid])
                 lens[r.rid] = r.prompt
-                torch.cuda.synchronize()
+                self.online_stream.synchronize()  # never a device-wide sync: a gated launch may be queued
                 t_pe = now_us()
                 log.add(t_pe, "prefill_end", **{"class": "online"}, request_id=r.rid, gpu=0)
                 self.res.prefill_us.append(t_pe - t_it)
@@ -456,7 +493,7 @@ class Colocation:
             toks = torch.randint(0, m.s.vocab, (len(decoding),), device=m.device)
             t_it = now_us()
             m.decode(toks, [caches[r.rid] for r in decoding], [lens[r.rid] for r in decoding])
-            torch.cuda.synchronize()
+            self.online_stream.synchronize()  # never a device-wide sync: a gated launch may be queued
             t_emit = now_us()
             self.res.decode_iter_us.append(t_emit - t_it)
             done = []
@@ -478,7 +515,7 @@ class Colocation:
                 self.res.ttft_us[r.rid] = r.first_us - r.arrival_us
                 log.add(t_emit, "done", **{"class": "online"}, request_id=r.rid, gpu=0, tokens=len(r.emits),
                         first_token_us=r.emits[0], last_token_us=r.emits[-1], digest="0x0000000000000000")
-        torch.cuda.synchronize()
+        self.online_stream.synchronize()  # never a device-wide sync: a gated launch may be queued
         self.res.wall_s = time.perf_counter() - t0
         if busy:
             log.add(now_us(), "busy", gpu=0, **{"class": "online"}, start_us=busy_since, end_us=now_us())
@@ -490,9 +527,15 @@ class Colocation:
             gen = self.channel.disables_issued() + 1000
             self.gate.raise_(gen)
             self.gate.wait_quiesced(gen)
-            torch.cuda.synchronize()
+            # not a device-wide sync here: an offline launch already queued behind "gate open"
+            # would wait for the release below forever
+            torch.cuda.ExternalStream(self.gate.stream).synchronize()
             self.res.offline_tiles = self._harvest + self.gate.read().tiles_done
             self.res.offline_bytes = self.res.offline_tiles * self.tile_bytes
+            if self.gemm_gate is not None:
+                m, n, k = self.gemm_shape
+                self.res.offline_gemm_tiles = self._gemm_harvest + self.gemm_gate.read().tiles_done
+                self.res.offline_gemm_flop = self.res.offline_gemm_tiles * 2.0 * m * n * k / self.gemm_tiles
             self.gate.release(gen)
             torch.cuda.synchronize()
         return self.res
@@ -531,6 +574,51 @@ def warm_shapes(model: OnlineModel, trace: List[OnlineReq]):
     torch.cuda.synchronize()
 
 
+class _Clocks:
+    """nvidia-smi SM clock / power samples (100 ms) over one run -- evidence for clock effects of
+    the offline tenant (a tensor-heavy tenant in the gaps can push the GPU into its power cap)."""
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        import subprocess
+        import threading
+
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,power.draw",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            try:
+                self.rows.append(tuple(float(x) for x in line.split(",")))
+            except ValueError:
+                pass
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return None
+        sm = sorted(r[0] for r in self.rows)
+        pw = sorted(r[1] for r in self.rows)
+        return {"sm_mhz_median": sm[len(sm) // 2], "sm_mhz_min": sm[0], "power_w_median": pw[len(pw) // 2],
+                "power_w_max": pw[-1], "samples": len(sm)}
+
+
 def _avg_runs(dicts):
     """Per-request mean over runs (requests present in every run)."""
     keys = set(dicts[0])
@@ -541,6 +629,7 @@ def _avg_runs(dicts):
 
 def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, handles=64, seed=2604,
                    output=(8, 12), prompt=(2500, 3500), layers=32, device=0, offline_ctas=0, repeats=1,
+                   offline_gemm=None,
                    log_dir: Optional[str] = None):
     """Paired standalone vs colocated run of one online trace (default: the pair_06 shape --
     spike base 0.3/s, 6/s for 1 s every 8 s, prompt 2500-3500, output 8-12 -- so the online
@@ -560,13 +649,18 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
     trace = spike_trace(seed, horizon, base, spike, period, width, prompt=prompt, output=output)
     warm_shapes(model, trace)
     solos, colos = [], []
+    clocks = {"standalone": [], "colocated": []}
     for i in range(repeats):
-        solos.append(Colocation(model, None, None).run(trace, horizon_s=horizon + 30))
+        with _Clocks(device) as ck:
+            solos.append(Colocation(model, None, None).run(trace, horizon_s=horizon + 30))
+        clocks["standalone"].append(ck.summary())
         pool = A.DevicePool(handles, 64, 16, device=device, slot_bytes=2 << 20, page_bytes=917504,
                             max_requests=4096, max_pages_per_request=1024)
         gate = A.Gate(device)
-        colo_rt = Colocation(model, pool, gate, offline_ctas=offline_ctas)
-        colos.append(colo_rt.run(trace, offline_population(seed, 4 * handles), horizon_s=horizon + 30))
+        colo_rt = Colocation(model, pool, gate, offline_ctas=offline_ctas, offline_gemm=offline_gemm)
+        with _Clocks(device) as ck:
+            colos.append(colo_rt.run(trace, offline_population(seed, 4 * handles), horizon_s=horizon + 30))
+        clocks["colocated"].append(ck.summary())
         del pool, gate, colo_rt
         import gc
 
@@ -625,12 +719,15 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         "reclaims": colo.reclaims, "reclaimed_handles": colo.reclaimed_handles,
         "offline_ctas": offline_ctas or "default",
         "offline_gbs_harvested": colo.offline_bytes / colo.wall_s / 1e9,
+        "offline_gemm": ({"shape": list(offline_gemm), "tflops_harvested": colo.offline_gemm_flop / colo.wall_s / 1e12,
+                          "tiles": colo.offline_gemm_tiles} if offline_gemm else None),
         "prefill_ms_median": {"standalone": _median([x for s in solos for x in s.prefill_us]) / 1e3,
                               "colocated": _median([x for c in colos for x in c.prefill_us]) / 1e3},
         "decode_iter_ms_median": {
             "standalone": _median([x for s in solos for x in s.decode_iter_us]) / 1e3,
             "colocated": _median([x for c in colos for x in c.decode_iter_us]) / 1e3},
         "wall_s": {"standalone": solos[0].wall_s, "colocated": colo.wall_s},
+        "clocks_per_run": clocks,
     }
     import gc
 

@@ -19,7 +19,9 @@ if __name__ == "__main__":
     ap.add_argument("--seed", type=int, default=2604)
     ap.add_argument("--repeats", type=int, default=2)
     ap.add_argument("--offline-ctas", type=int, default=148)
+    ap.add_argument("--gemm", default="", help="m,n,k of the gated offline GEMM tenant (empty: decode only)")
     a = ap.parse_args()
+    gemm = tuple(int(x) for x in a.gemm.split(",")) if a.gemm else None
     print(json.dumps(RT.measure_deltas(a.horizon, a.base, a.spike, handles=a.handles, layers=a.layers,
                                        seed=a.seed, repeats=a.repeats,
-                                       offline_ctas=a.offline_ctas)))
+                                       offline_ctas=a.offline_ctas, offline_gemm=gemm)))

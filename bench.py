@@ -60,8 +60,9 @@ def parse():
     ap.add_argument("--tma", type=int, default=0)
     ap.add_argument("--seed", type=int, default=2604)
     ap.add_argument("--skip-realtime", action="store_true", help="skip the measured TTFT/TPOT run")
+    ap.add_argument("--skip-fanout", action="store_true", help="skip the same-device TP fan-out sweep")
     ap.add_argument("--rt-horizon", type=float, default=24.0, help="online trace length (s)")
-    ap.add_argument("--rt-repeats", type=int, default=2, help="colocated runs (interleaved with standalone)")
+    ap.add_argument("--rt-repeats", type=int, default=3, help="colocated runs (interleaved with standalone)")
     ap.add_argument("--rt-gemm", default="2048,37888,3584",
                     help="m,n,k of the offline tenant's gated tcgen05 GEMM (Qwen2-7B gate/up); '' = decode pass only")
     ap.add_argument("--profile-mode", action="store_true",
@@ -291,6 +292,51 @@ def gemm_tenant(torch, A, gate, dev, stream, gate_stream, preemptions, next_gen)
             "max_quiesce_us": q[-1] if q else None}
 
 
+def tp_fanout_same_device(torch, A, pool, dev, groups=(1, 2, 4, 8), iters=300, seed=0, mode=0):
+    """TP-group gate fan-out with every member gate on this one GPU: the leader's
+    raise writes all N gate words (stream memory operations), its wait joins N concurrent
+    live_ctas waits on helper streams; each member runs its own gated offline kernel on 148/N
+    CTAs.  Measures how preempt-to-quiesce scales with the group size for the fan-out mechanism
+    itself (the reference's unpatched toggle is linear in GPUs, scenario.hpp:56-58).  Caveat: the
+    members share one device, so the NVLink hop of a real TP group is not in these numbers."""
+    rng = random.Random(seed)
+    out = {}
+    for n in groups:
+        gates = [A.Gate(dev.index) for _ in range(n)]
+        gates[0].set_fanout(mode)
+        if n > 1:
+            gates[0].attach_peers(gates[1:])
+        streams = [torch.cuda.Stream(device=dev) for _ in range(n)]
+        gs = torch.cuda.ExternalStream(gates[0].stream, device=dev)
+        ctas = max(1, 148 // n)
+        lat = []
+        for it in range(iters + 20):
+            for g, st in zip(gates, streams):
+                g.reset_work()  # a fresh pass each time (one pass is far longer than a sample)
+                g.launch_offline(pool, None, None, 0, 0, None, ctas=ctas, stream=st.cuda_stream)
+            deadline = time.perf_counter() + rng.uniform(100e-6, 400e-6)
+            while time.perf_counter() < deadline:
+                pass
+            gen = it + 1
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(gs)
+            gates[0].raise_(gen)
+            gates[0].wait_quiesced(gen)
+            e1.record(gs)
+            gates[0].release(gen)
+            e1.synchronize()
+            if it >= 20:
+                lat.append(e0.elapsed_time(e1) * 1e3)
+        torch.cuda.synchronize()
+        lat.sort()
+        out[str(n)] = {"p50_us": round(lat[len(lat) // 2], 2), "p99_us": round(lat[int(0.99 * (len(lat) - 1))], 2),
+                       "max_us": round(lat[-1], 2), "preemptions": len(lat), "ctas_per_member": ctas}
+        del gates
+    return {"note": "one leader + N-1 member gates on one B200 (no NVLink hop); offline decode pass "
+                    "per member on 148/N CTAs; leader raise -> all members quiesced",
+            "ack_wait": ["batched memops on the waiting stream", "helper stream per member"][mode], "groups": out}
+
+
 def run_valve(args, rank, world, dist):
     import torch
 
@@ -313,7 +359,8 @@ def run_valve(args, rank, world, dist):
     gate_stream = torch.cuda.ExternalStream(gate.stream, device=dev)
     pool_stream = torch.cuda.ExternalStream(pool.view().stream, device=dev)
     cap_pages = args.k * HSZ
-    host = A.HostBuffer(cap_pages * PAGE)
+    hosts = [A.HostBuffer(cap_pages * PAGE), A.HostBuffer(cap_pages * PAGE)]  # two copies in flight
+    host = hosts[0]
     cp = A.copy_params(ctas=args.copy_ctas, threads=args.copy_threads, use_tma=args.tma)
     peak = link_peak_d2h(torch, dev)
     gen = [0]
@@ -350,7 +397,27 @@ def run_valve(args, rank, world, dist):
         total = sum(p for p, _ in live.values()) * (-(-PAGE // TILE))
         return gate.read().tiles_claimed >= 0.8 * total
 
+    pending = []  # copies in flight (FIFO): (record, pages)
+
+    def drain(keep):
+        """Complete copies until at most `keep` are in flight; returns their bytes."""
+        done = 0
+        while len(pending) > keep:
+            rec, npg_ = pending.pop(0)
+            cs = pool.reclaim_copy_wait()
+            done += cs.bytes
+            if rec:
+                stats["copy_ms"].append(cs.kernel_ms)
+                stats["bytes"].append(cs.bytes)
+                stats["pages"].append(npg_)
+        return done
+
     def step(record):
+        """One reclaim op: raise -> quiesce -> fused select/apply -> start the gather copy ->
+        re-admit -> release.  The gate only has to cover the remap (after apply the offline block
+        tables no longer reach the reclaimed slots), and the copy works from its own snapshot of
+        the report, so op i+1's quiesce and decision overlap op i's bytes on the link: one copy
+        stays queued behind the running one and the link never idles between ops."""
         nonlocal t
         if tiles_left_low():  # offline work list exhausted: start a new pass
             gate.reset_work()
@@ -368,21 +435,22 @@ def run_valve(args, rank, world, dist):
         nh, ne, npg = pool.reclaim(args.k, t, 0)
         e3.record(pool_stream)
         res = pool.last_reclaim()
-        pool.reclaim_copy_start(host.ptr, host.nbytes, cp)  # copy overlaps the restore
+        pool.reclaim_copy_start(hosts[step.n % 2].ptr, hosts[0].nbytes, cp)
+        step.n += 1
+        pending.append((record, npg))
         restore(res.evicted_requests)
-        cs = pool.reclaim_copy_wait()
         gate.release(gen[0])
+        done = drain(1)
         if record:
             torch.cuda.synchronize()
             stats["quiesce_us"].append(e0.elapsed_time(e1) * 1e3)
             stats["reclaim_ms"].append(e2.elapsed_time(e3))
-            stats["copy_ms"].append(cs.kernel_ms)
-            stats["bytes"].append(cs.bytes)
-            stats["pages"].append(npg)
-        return cs.bytes
+        return done
+    step.n = 0
 
     for _ in range(args.warmup):
         step(False)
+    drain(0)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -394,6 +462,7 @@ def run_valve(args, rank, world, dist):
         total_bytes = 0
         for _ in range(args.steps):
             total_bytes += step(True)
+        total_bytes += drain(0)
         t1.record(pool_stream)
         torch.cuda.synchronize()
     launches = A.kernel_launches() - launches0
@@ -443,6 +512,13 @@ def run_valve(args, rank, world, dist):
         polled = max(rates[True])
         unpolled = max(rates[False])
 
+    # ------------------------------------------------ TP-group gate fan-out, one device
+    fanout = None
+    if not args.profile_mode and not args.skip_fanout and world == 1:
+        fanout = tp_fanout_same_device(torch, A, pool, dev, seed=args.seed)
+        fanout["alt_helper_streams"] = tp_fanout_same_device(torch, A, pool, dev, groups=(2, 4, 8), iters=200,
+                                                             seed=args.seed, mode=1)["groups"]
+
     # ------------------------------------------------ GEMM tenant (tcgen05)
     def next_gen():
         gen[0] += 1
@@ -474,12 +550,16 @@ def run_valve(args, rank, world, dist):
                               "reduction_pct": round((1 - sel_c / fifo_c) * 100, 2) if fifo_c else None}
 
     # ------------------------------------------------ e2e through the reference-facing API
+    # one copy stays in flight behind the running one (as in step()): op i+1's quiesce, snapshot,
+    # selection and apply run on the host/pool stream while op i's bytes cross the link
     e2e_bytes = e2e_h2d = e2e_d2h = 0
     brk = {"quiesce": 0.0, "snapshot": 0.0, "select": 0.0, "apply": 0.0, "restore": 0.0, "copy_wait": 0.0}
+    n_e2e = max(1, args.steps)
     torch.cuda.synchronize()
     w0 = time.perf_counter()
-    for it in range(max(1, args.steps // 2) + 1):  # iteration 0 is an untimed warm-up
+    for it in range(n_e2e + 1):  # iteration 0 is an untimed warm-up
         if it == 1:
+            e2e_bytes += drain(0)
             torch.cuda.synchronize()
             w0 = time.perf_counter()
             e2e_bytes = e2e_h2d = e2e_d2h = 0
@@ -491,7 +571,7 @@ def run_valve(args, rank, world, dist):
         gate.raise_(gen[0])
         gate.wait_quiesced(gen[0])
         torch.cuda.current_stream().wait_stream(gate_stream)
-        torch.cuda.synchronize()
+        torch.cuda.current_stream().synchronize()
         p1 = time.perf_counter()
         inst = pool.snapshot()                                   # D2H instance
         inst.cost = {r: live[r][1] for h in inst.handles for r in h.requests}
@@ -502,31 +582,32 @@ def run_valve(args, rank, world, dist):
         p3 = time.perf_counter()
         res = pool.apply_reclaim(ids, t)                         # H2D ids, D2H result
         npg = sum(len(v) for v in res.invalidated_pages.values())
-        pool.reclaim_copy_start(host.ptr, host.nbytes, cp)       # D2H page bytes
+        pool.reclaim_copy_start(hosts[it % 2].ptr, hosts[0].nbytes, cp)  # D2H page bytes
+        pending.append((False, npg))
         p4 = time.perf_counter()
         restore(res.evicted_requests)
-        p5 = time.perf_counter()
-        cs = pool.reclaim_copy_wait()
         gate.release(gen[0])
+        p5 = time.perf_counter()
+        e2e_bytes += drain(1)
         p6 = time.perf_counter()
         for key, a, b in (("quiesce", p0, p1), ("snapshot", p1, p2), ("select", p2, p3),
                           ("apply", p3, p4), ("restore", p4, p5), ("copy_wait", p5, p6)):
             brk[key] += (b - a) * 1e3
         n = len(inst.handles)
         m = len(inst.cost)
-        e2e_d2h += n * 16 + 4 + nnz * 8 + 4 * len(ids) + len(res.evicted_requests) * 12 + npg * 16 + cs.bytes
+        e2e_d2h += n * 16 + 4 + nnz * 8 + 4 * len(ids) + len(res.evicted_requests) * 12 + npg * 16
+        e2e_d2h += npg * PAGE  # the page bytes this op copies
         e2e_h2d += n * 16 + 4 + nnz * 8 + m * 16 + 4 * len(ids)
-        e2e_bytes += cs.bytes
+    e2e_bytes += drain(0)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - w0
-    n_e2e = max(1, args.steps // 2)
 
     copy_gbs = statistics.mean(b / (ms * 1e-3) / 1e9 for b, ms in zip(stats["bytes"], stats["copy_ms"]))
 
     # ------------------------------------------------ C3: weight pages (configs[2] mechanism)
     import gc
 
-    del pool, host
+    del pool, host, hosts
     gc.collect()
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -595,6 +676,7 @@ def run_valve(args, rank, world, dist):
         "offline_polling_overhead_pct": round((1 - polled[0] / unpolled[0]) * 100, 2),
         "offline_gbs": {"polled": round(polled[0], 1), "unpolled": round(unpolled[0], 1)},
         "offline_gemm": gemm,
+        "tp_fanout_same_device": fanout,
         "policy_contrast_recompute": contrast,
         "c3_weight_pages": c3,
         "ttft_delta_pct": rt.get("ttft_delta_pct"),
@@ -620,8 +702,9 @@ def run_valve(args, rank, world, dist):
             "unit": "GB/s",
             "h2d_bytes_per_step": int(e2e_h2d / n_e2e),
             "d2h_bytes_per_step": int(e2e_d2h / n_e2e),
-            "path": "snapshot() -> selective_reclaim(instance) -> apply_reclaim(ids) -> copy, host buffers",
-            "breakdown_ms_per_step": {k: round(v / max(1, args.steps // 2), 3) for k, v in brk.items()},
+            "path": "snapshot() -> selective_reclaim(instance) -> apply_reclaim(ids) -> reclaim_copy_start(), host buffers",
+            "breakdown_ms_per_step": {k: round(v / n_e2e, 3) for k, v in brk.items()},
+            "pipelining": "one reclaim copy queued behind the running one (op i+1 decides while op i copies)",
         },
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),

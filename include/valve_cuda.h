@@ -147,9 +147,12 @@ void valve_copy_params_default(valve_copy_params* c);
  * Synchronous. */
 int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
                             const valve_copy_params* params, valve_copy_stats* stats);
-/* Asynchronous form: the copy runs on the pool's copy stream, ordered after the report, while
- * bookkeeping calls (reserve/release/grow/...) proceed on the pool stream; the next
- * apply_reclaim / reclaim / fill_pages waits for it automatically.  One copy in flight. */
+/* Asynchronous form: the copy runs on the pool's copy stream, ordered after the report, and
+ * works from its own device snapshot of the report, so bookkeeping calls (reserve/release/
+ * grow/...) and the NEXT apply_reclaim / reclaim proceed on the pool stream while the bytes
+ * cross the link (back-to-back reclaim ops keep the link busy).  fill_pages / restore wait for
+ * the copy (they rewrite page bytes).  Up to two copies in flight; each _wait completes the
+ * oldest one (FIFO) and returns its stats.  The synchronous form requires none in flight. */
 int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_bytes,
                                   const valve_copy_params* params);
 int valve_pool_reclaim_copy_wait(valve_pool* p, valve_copy_stats* stats);
@@ -242,6 +245,12 @@ int valve_gate_raise_stamped(valve_gate* g, uint32_t gen, void* stream);
 int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* stream);
 /* TP fan-out: members' gate words are written by the leader over NVLink peer memory. */
 int valve_gate_attach_peers(valve_gate* leader, valve_gate** members, int n);
+/* How the leader waits for the members' acks: BATCHED (default) = one stream-memory-operation
+ * submission on the waiting stream (members' counters checked in order; all members started
+ * quiescing at the raise); STREAMS = one helper stream per member joined by events. */
+#define VALVE_FANOUT_BATCHED 0
+#define VALVE_FANOUT_STREAMS 1
+int valve_gate_set_fanout(valve_gate* g, int mode);
 /* One process per GPU: a member exports its gate words (CUDA IPC, 64-byte handle) and the
  * leader opens them as a remote gate (no kernels, words only) to pass to attach_peers. */
 #define VALVE_GATE_HANDLE_BYTES 64

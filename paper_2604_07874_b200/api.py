@@ -702,6 +702,7 @@ def _declare_valve_extras(L):
         "valve_gate_raise_stamped": (C.c_int, [vp, u32, vp]),
         "valve_gate_wait_quiesced": (C.c_int, [vp, u32, vp]),
         "valve_gate_attach_peers": (C.c_int, [vp, P(vp), C.c_int]),
+        "valve_gate_set_fanout": (C.c_int, [vp, C.c_int]),
         "valve_gate_export": (C.c_int, [vp, C.c_char_p]),
         "valve_gate_open_remote": (C.c_int, [C.c_int, C.c_char_p, P(vp)]),
         "valve_gate_read": (C.c_int, [vp, P(GateState)]),
@@ -897,6 +898,12 @@ class Gate:
         buf = C.create_string_buffer(self.HANDLE_BYTES)
         self._b.check(self._b.lib.valve_gate_export(self._h, buf))
         return buf.raw
+
+    FANOUT_BATCHED, FANOUT_STREAMS = 0, 1
+
+    def set_fanout(self, mode: int):
+        """Leader's ack wait: FANOUT_BATCHED (one memop submission, default) or FANOUT_STREAMS."""
+        self._b.check(self._b.lib.valve_gate_set_fanout(self._h, int(mode)))
 
     def attach_peers(self, members: Sequence["Gate"]):
         """TP fan-out: raise/release/wait on this (leader) gate also drive the members' words."""

@@ -59,10 +59,12 @@ void counted() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 using PFN_write32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 using PFN_wait32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 using PFN_write64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+using PFN_batch = CUresult (*)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
 struct MemOps {
   PFN_write32 write32 = nullptr;
   PFN_wait32 wait32 = nullptr;
   PFN_write64 write64 = nullptr;
+  PFN_batch batch = nullptr;
 };
 const MemOps& memops() {
   static MemOps ops;
@@ -72,8 +74,9 @@ const MemOps& memops() {
     cudaGetDriverEntryPoint("cuStreamWriteValue32", (void**)&ops.write32, cudaEnableDefault, &q);
     cudaGetDriverEntryPoint("cuStreamWaitValue32", (void**)&ops.wait32, cudaEnableDefault, &q);
     cudaGetDriverEntryPoint("cuStreamWriteValue64", (void**)&ops.write64, cudaEnableDefault, &q);
+    cudaGetDriverEntryPoint("cuStreamBatchMemOp", (void**)&ops.batch, cudaEnableDefault, &q);
   });
-  if (!ops.write32 || !ops.wait32 || !ops.write64)
+  if (!ops.write32 || !ops.wait32 || !ops.write64 || !ops.batch)
     fail(VALVE_CUDA_ERROR, "stream memory operations unavailable in this driver");
   return ops;
 }
@@ -125,14 +128,33 @@ struct valve_pool {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaStream_t copy_stream = nullptr;  // reclaim copies overlap pool bookkeeping
   cudaEvent_t ev_report = nullptr;
-  unsigned long long* d_copyctr = nullptr;
-  bool copy_pending = false;
-  int64_t copy_bytes = 0, copy_pages = 0;
+  unsigned long long* d_copyctr = nullptr;  // restore / copy-engine counters (pool stream)
+  // Reclaim copies in flight (FIFO ring).  Each copy first snapshots the report it needs (the
+  // physical page list, plus the byte layout for per-request page sizes) into its own slot on
+  // the copy stream, so the next decision may rewrite the report while the bytes are still
+  // crossing the link: back-to-back reclaim ops keep the host link busy.
+  struct CopySlot {
+    int* phys = nullptr;
+    int* inv_off = nullptr;
+    int64_t* ev_pbytes = nullptr;
+    int64_t* ev_base = nullptr;
+    int64_t* ev_cbase = nullptr;
+    unsigned long long* ctr = nullptr;  // cursor, t_first, t_last
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_plan = nullptr;
+    int64_t bytes = 0, pages = 0;
+  };
+  static constexpr int kCopySlots = 2;
+  CopySlot cs[kCopySlots];
+  int cs_head = 0, cs_n = 0, cs_last = -1;
 
-  // Kernels that rewrite the report (apply/reclaim) or page bytes (fill) must not overtake an
-  // in-flight copy of the previous report.
+  // Kernels that rewrite the report (apply/reclaim) must not overtake the report snapshot of
+  // the latest copy; kernels that rewrite page bytes (fill, restore) must not overtake the copy
+  // itself.  Copies run in order on the copy stream, so the latest one covers the earlier ones.
+  void order_after_copy_plan() {
+    if (cs_last >= 0) ck(cudaStreamWaitEvent(stream, cs[cs_last].ev_plan, 0), "event wait");
+  }
   void order_after_copy() {
-    if (ev1) ck(cudaStreamWaitEvent(stream, ev1, 0), "event wait");
+    if (cs_last >= 0) ck(cudaStreamWaitEvent(stream, cs[cs_last].ev1, 0), "event wait");
   }
 
   template <class T>
@@ -189,6 +211,10 @@ struct valve_pool {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev_report) cudaEventDestroy(ev_report);
+    for (CopySlot& c : cs)
+      for (cudaEvent_t e : {c.ev0, c.ev1, c.ev_plan})
+        if (e) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamSynchronize(copy_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -294,6 +320,17 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   p->d_in64 = p->dalloc<int64_t>(R);
   p->d_in64b = p->dalloc<int64_t>(R);
   p->d_copyctr = p->dalloc<unsigned long long>(4);
+  for (auto& cs : p->cs) {
+    cs.phys = p->dalloc<int>(HS);
+    cs.inv_off = p->dalloc<int>(R + 1);
+    cs.ev_pbytes = p->dalloc<int64_t>(R);
+    cs.ev_base = p->dalloc<int64_t>(R + 1);
+    cs.ev_cbase = p->dalloc<int64_t>(R + 1);
+    cs.ctr = p->dalloc<unsigned long long>(4);
+    ck(cudaEventCreate(&cs.ev0), "cudaEventCreate");
+    ck(cudaEventCreate(&cs.ev1), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&cs.ev_plan, cudaEventDisableTiming), "cudaEventCreate");
+  }
   d.slot_bytes = c.slot_bytes;
   d.page_bytes = c.page_bytes;
   if (c.slot_bytes > 0) {
@@ -498,6 +535,7 @@ int valve_pool_request_row(const valve_pool* cp, int64_t req, int* row) {
 int valve_pool_block_table(const valve_pool* cp, int64_t req, int* out, int cap, int* n) {
   auto* p = const_cast<valve_pool*>(cp);
   return guard([&] {
+    p->order_after_copy_plan();  // the page list is written into the report buffer
     p->launch1("block_table", k_block_table, 0, p->d, req, p->d.res_phys);
     *n = (int)p->mirror->r[0];
     if (out) p->d2h(out, p->d.res_phys, (size_t)std::min(*n, cap) * 4);
@@ -535,7 +573,7 @@ int valve_pool_apply_reclaim(valve_pool* p, const int* ids, int k, int64_t t, in
     ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
     if (k) ck(cudaMemcpyAsync(p->d_ids, ids, (size_t)k * 4, cudaMemcpyHostToDevice, p->stream), "upload ids");
     try {
-      p->order_after_copy();
+      p->order_after_copy_plan();
       p->launch1("apply_reclaim", k_apply, p->smem_reclaim, p->d, (const int*)p->d_ids, k, t);
     } catch (const Err&) {
       p->last_n_handles = (int)p->mirror->r[0];
@@ -639,7 +677,7 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
     if (k < 0) fail(VALVE_INVALID_ARGUMENT, "selective_reclaim: k must be >= 0");
     if (mode != VALVE_SELECT_SELECTIVE && mode != VALVE_SELECT_FIFO)
       fail(VALVE_INVALID_ARGUMENT, "reclaim: device-fused mode must be selective or fifo");
-    p->order_after_copy();
+    p->order_after_copy_plan();
     p->launch1("reclaim", k_reclaim, p->smem_reclaim, p->d, k, mode, t);
     p->last_n_handles = (int)p->mirror->r[0];
     p->last_n_evicted = (int)p->mirror->r[1];
@@ -725,7 +763,8 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
     if (!p->d.pages) fail(VALVE_LOGIC_ERROR, "reclaim_copy: pool has no page store");
     if (c.chunk_bytes % 16 || c.threads % 32 || c.threads > 512)
       fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: chunk must be a 16-byte multiple, threads <= 512");
-    if (p->copy_pending) fail(VALVE_LOGIC_ERROR, "reclaim_copy: a copy is already in flight");
+    if (p->cs_n == valve_pool::kCopySlots)
+      fail(VALVE_LOGIC_ERROR, "reclaim_copy: two copies already in flight (call reclaim_copy_wait)");
     const int64_t need = p->last_copy_bytes;
     if (dst_bytes < need) fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: destination too small");
     if (reinterpret_cast<uintptr_t>(host_dst) % 16)
@@ -735,40 +774,50 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
     void* ddst = nullptr;
     ck(cudaHostGetDevicePointer(&ddst, host_dst, 0),
        "reclaim_copy: destination is not pinned/mapped host memory");
+    const int si = (p->cs_head + p->cs_n) % valve_pool::kCopySlots;
+    valve_pool::CopySlot& S = p->cs[si];
+    const int n_pages = p->last_n_pages, n_ev = p->last_n_evicted;
     CopyArgs A{};
     A.pages = p->d.pages;
     A.slot_bytes = p->d.slot_bytes;
     A.page_bytes = p->d.page_bytes;
     A.chunk_bytes = c.chunk_bytes;
-    A.phys = p->d.res_phys;
-    A.n_pages = p->last_n_pages;
+    A.phys = S.phys;
+    A.n_pages = n_pages;
     const int64_t cpp = (A.page_bytes + c.chunk_bytes - 1) / c.chunk_bytes;
     A.n_chunks = (int64_t)A.n_pages * cpp;
     A.dst = static_cast<uint8_t*>(ddst);
     A.ns_per_byte = c.rate_bytes_per_s > 0 ? 1e9 / c.rate_bytes_per_s : 0.0;
     A.burst_bytes = c.burst_bytes;
-    unsigned long long* ctr = p->d_copyctr;
-    A.cursor = ctr;
-    A.t_first = ctr + 1;
-    A.t_last = ctr + 2;
-    // the copy runs on its own stream after the report exists; bookkeeping on the pool
-    // stream overlaps it, and the next apply/reclaim/fill waits for it (report + page bytes)
+    A.cursor = S.ctr;
+    A.t_first = S.ctr + 1;
+    A.t_last = S.ctr + 2;
+    // the copy runs on its own stream after the report exists and works from its own snapshot
+    // of it; bookkeeping and the next decision proceed on the pool stream meanwhile
     ck(cudaEventRecord(p->ev_report, p->stream), "event");
     ck(cudaStreamWaitEvent(p->copy_stream, p->ev_report, 0), "event wait");
-    ck(cudaMemsetAsync(ctr, 0, 24, p->copy_stream), "memset");
+    const cudaMemcpyKind d2d = cudaMemcpyDeviceToDevice;
+    if (n_pages) ck(cudaMemcpyAsync(S.phys, p->d.res_phys, (size_t)n_pages * 4, d2d, p->copy_stream), "snapshot");
+    if (custom && n_ev) {
+      ck(cudaMemcpyAsync(S.inv_off, p->d.res_inv_off, (size_t)(n_ev + 1) * 4, d2d, p->copy_stream), "snapshot");
+      ck(cudaMemcpyAsync(S.ev_pbytes, p->d.res_ev_pbytes, (size_t)n_ev * 8, d2d, p->copy_stream), "snapshot");
+      ck(cudaMemcpyAsync(S.ev_base, p->d.res_ev_base, (size_t)(n_ev + 1) * 8, d2d, p->copy_stream), "snapshot");
+    }
+    ck(cudaEventRecord(S.ev_plan, p->copy_stream), "event");
+    ck(cudaMemsetAsync(S.ctr, 0, 24, p->copy_stream), "memset");
     if (custom) {  // per-request page sizes: chunk prefix over the evicted requests first
-      A.ev_pbytes = p->d.res_ev_pbytes;
-      A.ev_base = p->d.res_ev_base;
-      A.ev_cbase = p->d.res_ev_cbase;
-      A.inv_off = p->d.res_inv_off;
-      A.n_ev = p->last_n_evicted;
-      A.n_chunks = p->last_n_evicted > 0 ? 1 : 0;  // the kernel reads the total from ev_cbase
+      A.ev_pbytes = S.ev_pbytes;
+      A.ev_base = S.ev_base;
+      A.ev_cbase = S.ev_cbase;
+      A.inv_off = S.inv_off;
+      A.n_ev = n_ev;
+      A.n_chunks = n_ev > 0 ? 1 : 0;  // the kernel reads the total from ev_cbase
       if (A.n_chunks) {
-        k_copy_plan<<<1, 1024, 0, p->copy_stream>>>(A.ev_pbytes, A.inv_off, A.n_ev, A.chunk_bytes, p->d.res_ev_cbase);
+        k_copy_plan<<<1, 1024, 0, p->copy_stream>>>(A.ev_pbytes, A.inv_off, A.n_ev, A.chunk_bytes, S.ev_cbase);
         counted();
       }
     }
-    ck(cudaEventRecord(p->ev0, p->copy_stream), "event");
+    ck(cudaEventRecord(S.ev0, p->copy_stream), "event");
     if (A.n_chunks > 0) {
       if (c.use_tma && !custom) {
         k_reclaim_copy_tma<<<c.ctas, 32, 2 * 32768, p->copy_stream>>>(A);
@@ -777,27 +826,30 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
       }
       counted();
     }
-    ck(cudaEventRecord(p->ev1, p->copy_stream), "event");
+    ck(cudaEventRecord(S.ev1, p->copy_stream), "event");
     ck(cudaGetLastError(), "reclaim_copy launch");
-    p->copy_pending = true;
-    p->copy_bytes = need;
-    p->copy_pages = p->last_n_pages;
+    S.bytes = need;
+    S.pages = n_pages;
+    p->cs_n++;
+    p->cs_last = si;
   });
 }
 
 int valve_pool_reclaim_copy_wait(valve_pool* p, valve_copy_stats* st) {
   return guard([&] {
-    if (!p->copy_pending) fail(VALVE_LOGIC_ERROR, "reclaim_copy_wait: no copy in flight");
+    if (!p->cs_n) fail(VALVE_LOGIC_ERROR, "reclaim_copy_wait: no copy in flight");
     ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
-    ck(cudaEventSynchronize(p->ev1), "reclaim_copy");
-    p->copy_pending = false;
+    valve_pool::CopySlot& S = p->cs[p->cs_head];
+    ck(cudaEventSynchronize(S.ev1), "reclaim_copy");
+    p->cs_head = (p->cs_head + 1) % valve_pool::kCopySlots;
+    p->cs_n--;
     if (st) {
       float ms = 0;
-      ck(cudaEventElapsedTime(&ms, p->ev0, p->ev1), "event");
+      ck(cudaEventElapsedTime(&ms, S.ev0, S.ev1), "event");
       unsigned long long t[3];
-      ck(cudaMemcpy(t, p->d_copyctr, 24, cudaMemcpyDeviceToHost), "read");
-      st->bytes = p->copy_bytes;
-      st->pages = p->copy_pages;
+      ck(cudaMemcpy(t, S.ctr, 24, cudaMemcpyDeviceToHost), "read");
+      st->bytes = S.bytes;
+      st->pages = S.pages;
       st->kernel_ms = ms;
       st->t_first_ns = t[1];
       st->t_last_ns = t[2];
@@ -807,6 +859,10 @@ int valve_pool_reclaim_copy_wait(valve_pool* p, valve_copy_stats* st) {
 
 int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
                             const valve_copy_params* prm, valve_copy_stats* st) {
+  if (p->cs_n) {
+    g_err = "reclaim_copy: a copy started with reclaim_copy_start is still in flight";
+    return VALVE_LOGIC_ERROR;
+  }
   const int rc = valve_pool_reclaim_copy_start(p, host_dst, dst_bytes, prm);
   if (rc != VALVE_OK) return rc;
   return valve_pool_reclaim_copy_wait(p, st);
@@ -1220,6 +1276,7 @@ struct valve_gate {
   // on the members' acks run concurrently (front-end waits are serial within a stream)
   std::vector<cudaStream_t> wait_streams;
   std::vector<cudaEvent_t> wait_events;
+  int fanout_mode = VALVE_FANOUT_BATCHED;
   ~valve_gate() {
     if (stream) cudaStreamSynchronize(stream);
     if (work_stream) {
@@ -1238,6 +1295,39 @@ struct valve_gate {
 namespace {
 cudaStream_t as_stream(void* s, cudaStream_t dflt) { return s ? static_cast<cudaStream_t>(s) : dflt; }
 CUdeviceptr dptr(const void* p) { return reinterpret_cast<CUdeviceptr>(p); }
+
+// One submission of stream memory operations (executed in array order by the front end).
+struct MemBatch {
+  std::vector<CUstreamBatchMemOpParams> ops;
+  void write32(const void* addr, uint32_t v) {
+    CUstreamBatchMemOpParams p{};
+    p.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+    p.writeValue.address = dptr(addr);
+    p.writeValue.value = v;
+    ops.push_back(p);
+  }
+  void write64(const void* addr, uint64_t v) {
+    CUstreamBatchMemOpParams p{};
+    p.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+    p.writeValue.address = dptr(addr);
+    p.writeValue.value64 = v;
+    ops.push_back(p);
+  }
+  void wait_eq32(const void* addr, uint32_t v) {
+    CUstreamBatchMemOpParams p{};
+    p.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+    p.waitValue.address = dptr(addr);
+    p.waitValue.value = v;
+    p.waitValue.flags = CU_STREAM_WAIT_VALUE_EQ;
+    ops.push_back(p);
+  }
+  void submit(const MemOps& op, cudaStream_t st) {
+    for (size_t i = 0; i < ops.size(); i += 256) {  // driver limit per call
+      const unsigned n = (unsigned)std::min<size_t>(256, ops.size() - i);
+      cu_ck(op.batch((CUstream)st, n, ops.data() + i, 0), "cuStreamBatchMemOp");
+    }
+  }
+};
 }  // namespace
 
 extern "C" {
@@ -1274,14 +1364,15 @@ int valve_gate_raise(valve_gate* g, uint32_t gen, void* s) {
     const MemOps& op = memops();
     cudaStream_t st = as_stream(s, g->stream);
     ck(cudaSetDevice(g->device), "cudaSetDevice");
-    // leader first, then the TP members' words over peer memory (flat fan-out)
-    std::vector<valve_gate*> all{g};
-    all.insert(all.end(), g->peers.begin(), g->peers.end());
-    for (valve_gate* x : all) {
-      cu_ck(op.write64((CUstream)st, dptr(&x->d->t_first_seen), 0, 0), "cuStreamWriteValue64");
-      cu_ck(op.write32((CUstream)st, dptr(&x->d->gen), gen, 0), "cuStreamWriteValue32");
-      cu_ck(op.write32((CUstream)st, dptr(&x->d->closed), 1, 0), "cuStreamWriteValue32");
-    }
+    // one submission: every member's `closed` word first (leader, then the TP members over peer
+    // memory -- a flat fan-out), the diagnostic generation after (t_first_seen is cleared at
+    // release, while nothing polls)
+    MemBatch b;
+    b.write32(&g->d->closed, 1);
+    for (valve_gate* x : g->peers) b.write32(&x->d->closed, 1);
+    b.write32(&g->d->gen, gen);
+    for (valve_gate* x : g->peers) b.write32(&x->d->gen, gen);
+    b.submit(op, st);
   });
 }
 
@@ -1302,10 +1393,13 @@ int valve_gate_release(valve_gate* g, uint32_t gen, void* s) {
     ck(cudaSetDevice(g->device), "cudaSetDevice");
     std::vector<valve_gate*> all{g};
     all.insert(all.end(), g->peers.begin(), g->peers.end());
+    MemBatch b;
     for (valve_gate* x : all) {
-      cu_ck(op.write32((CUstream)st, dptr(&x->d->gen), gen, 0), "cuStreamWriteValue32");
-      cu_ck(op.write32((CUstream)st, dptr(&x->d->closed), 0, 0), "cuStreamWriteValue32");
+      b.write64(&x->d->t_first_seen, 0);
+      b.write32(&x->d->gen, gen);
     }
+    for (valve_gate* x : all) b.write32(&x->d->closed, 0);
+    b.submit(op, st);
   });
 }
 
@@ -1314,7 +1408,18 @@ int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* s) {
     const MemOps& op = memops();
     cudaStream_t st = as_stream(s, g->stream);
     ck(cudaSetDevice(g->device), "cudaSetDevice");
-    // members first, each on its own helper stream (concurrent), joined into `st` by events
+    if (g->fanout_mode == VALVE_FANOUT_BATCHED || g->peers.empty()) {
+      // one submission on `st`: the waits run in order, but every member started quiescing at
+      // the raise, so each later wait finds its counter already at zero (cost ~ max, not sum)
+      MemBatch b;
+      b.wait_eq32(&g->d->live_ctas, 0);
+      for (valve_gate* x : g->peers) b.wait_eq32(&x->d->live_ctas, 0);
+      b.write32(&g->d->quiesced_gen, gen);
+      for (valve_gate* x : g->peers) b.write32(&x->d->quiesced_gen, gen);
+      b.submit(op, st);
+      return;
+    }
+    // VALVE_FANOUT_STREAMS: members on their own helper streams (concurrent), joined by events
     for (size_t i = 0; i < g->peers.size(); ++i) {
       cudaStream_t ws = g->wait_streams[i];
       ck(cudaEventRecord(g->wait_events[2 * i], st), "event");  // order after the raise on st
@@ -1328,6 +1433,14 @@ int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* s) {
     cu_ck(op.write32((CUstream)st, dptr(&g->d->quiesced_gen), gen, 0), "cuStreamWriteValue32");
     for (size_t i = 0; i < g->peers.size(); ++i)
       ck(cudaStreamWaitEvent(st, g->wait_events[2 * i + 1], 0), "event wait");
+  });
+}
+
+int valve_gate_set_fanout(valve_gate* g, int mode) {
+  return guard([&] {
+    if (mode != VALVE_FANOUT_BATCHED && mode != VALVE_FANOUT_STREAMS)
+      fail(VALVE_INVALID_ARGUMENT, "gate_set_fanout: mode must be VALVE_FANOUT_BATCHED or VALVE_FANOUT_STREAMS");
+    g->fanout_mode = mode;
   });
 }
 

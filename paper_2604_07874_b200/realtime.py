@@ -232,7 +232,7 @@ class RunResult:
 class Colocation:
     def __init__(self, model: OnlineModel, pool: Optional[A.DevicePool], gate: Optional[A.Gate],
                  page_tokens: int = 16, max_gap_us: int = 300, resparams: Optional[A.ReservationParams] = None,
-                 tile_bytes: int = 16384, offline_ctas: int = 0, offline_gemm=None):
+                 tile_bytes: int = 16384, offline_ctas: int = 0, offline_gemm=None, offline_gemm_ctas: int = 0):
         """offline_gemm=(m, n, k): the offline tenant also runs the gated tcgen05 GEMM (its
         projection work, e.g. Qwen2-7B gate/up over m tokens) next to the decode pass, on its own
         gate attached to the channel's gate, so one raise quiesces both."""
@@ -248,6 +248,7 @@ class Colocation:
         self.seq = 0
         self.offline_running = False
         self.gemm_gate = None
+        self.gemm_ctas = offline_gemm_ctas  # 0 = one CTA per SM (power knob: fewer SMs, less draw)
         if self.colocated and offline_gemm:
             m, n, k = offline_gemm
             dev = model.device
@@ -295,7 +296,7 @@ class Colocation:
             self._gemm_harvest += st.tiles_done
         m, n, k = self.gemm_shape
         self.gemm_gate.launch_gemm(self.gemm_a.data_ptr(), self.gemm_b.data_ptr(), self.gemm_c.data_ptr(),
-                                   m, n, k, stream=self.gemm_stream.cuda_stream, fresh=fresh)
+                                   m, n, k, ctas=self.gemm_ctas, stream=self.gemm_stream.cuda_stream, fresh=fresh)
 
     def _launch_decode(self):
         st = self.gate.read()
@@ -627,9 +628,25 @@ def _avg_runs(dicts):
     return {k: sum(d[k] for d in dicts) / len(dicts) for k in sorted(keys)}
 
 
+def _med_runs(dicts):
+    """Per-request median over runs (requests present in every run).  A wall-clock loop admits
+    an arrival at the first iteration boundary after it, so a few microseconds of jitter can move
+    a 45 ms prefill between two decode tokens of the batch and shift that request's TPOT by
+    several ms in one run; the median over runs discards such a flip, the mean keeps 1/n of it."""
+    keys = set(dicts[0])
+    for d in dicts[1:]:
+        keys &= set(d)
+    out = {}
+    for k in sorted(keys):
+        v = sorted(d[k] for d in dicts)
+        n = len(v)
+        out[k] = v[n // 2] if n % 2 else 0.5 * (v[n // 2 - 1] + v[n // 2])
+    return out
+
+
 def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, handles=64, seed=2604,
                    output=(8, 12), prompt=(2500, 3500), layers=32, device=0, offline_ctas=0, repeats=1,
-                   offline_gemm=None,
+                   offline_gemm=None, offline_gemm_ctas: int = 0,
                    log_dir: Optional[str] = None):
     """Paired standalone vs colocated run of one online trace (default: the pair_06 shape --
     spike base 0.3/s, 6/s for 1 s every 8 s, prompt 2500-3500, output 8-12 -- so the online
@@ -657,7 +674,8 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         pool = A.DevicePool(handles, 64, 16, device=device, slot_bytes=2 << 20, page_bytes=917504,
                             max_requests=4096, max_pages_per_request=1024)
         gate = A.Gate(device)
-        colo_rt = Colocation(model, pool, gate, offline_ctas=offline_ctas, offline_gemm=offline_gemm)
+        colo_rt = Colocation(model, pool, gate, offline_ctas=offline_ctas, offline_gemm=offline_gemm,
+                             offline_gemm_ctas=offline_gemm_ctas)
         with _Clocks(device) as ck:
             colos.append(colo_rt.run(trace, offline_population(seed, 4 * handles), horizon_s=horizon + 30))
         clocks["colocated"].append(ck.summary())
@@ -677,15 +695,18 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         for i, r in enumerate(colos):
             r.log.write_jsonl(os.path.join(log_dir, f"colo{i}.jsonl"))
 
-    base_ttft = _avg_runs([s.ttft_us for s in solos])
-    base_tpot = _avg_runs([s.tpot_us for s in solos])
-    colo_ttft = _avg_runs([c.ttft_us for c in colos])
-    colo_tpot = _avg_runs([c.tpot_us for c in colos])
+    base_ttft = _med_runs([s.ttft_us for s in solos])
+    base_tpot = _med_runs([s.tpot_us for s in solos])
+    colo_ttft = _med_runs([c.ttft_us for c in colos])
+    colo_tpot = _med_runs([c.tpot_us for c in colos])
     ttft = paired_increase(base_ttft, colo_ttft)
     tpot = paired_increase(base_tpot, colo_tpot)
+    # the same pairing on per-request run means (sensitive to single-run batching flips)
+    ttft_mean = paired_increase(_avg_runs([s.ttft_us for s in solos]), _avg_runs([c.ttft_us for c in colos]))
+    tpot_mean = paired_increase(_avg_runs([s.tpot_us for s in solos]), _avg_runs([c.tpot_us for c in colos]))
     even, odd = solos[0::2], solos[1::2]
-    aa_ttft = paired_increase(_avg_runs([s.ttft_us for s in even]), _avg_runs([s.ttft_us for s in odd]))
-    aa_tpot = paired_increase(_avg_runs([s.tpot_us for s in even]), _avg_runs([s.tpot_us for s in odd]))
+    aa_ttft = paired_increase(_med_runs([s.ttft_us for s in even]), _med_runs([s.ttft_us for s in odd]))
+    aa_tpot = paired_increase(_med_runs([s.tpot_us for s in even]), _med_runs([s.tpot_us for s in odd]))
     mech_ttft = _avg_runs([c.mech_ttft_us for c in colos]) if colos else {}
     mech_tpot = _avg_runs([c.mech_tpot_us for c in colos]) if colos else {}
     colo = colos[-1]
@@ -697,11 +718,13 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         "trace": {"horizon_s": horizon, "online_requests": len(trace), "base_rate": base, "spike_rate": spike,
                   "period_s": period, "width_s": width, "prompt": list(prompt), "output": list(output),
                   "model": f"Llama-3-8B-shaped, {layers} layers, random init bf16"},
-        "design": f"interleaved A/B x{repeats} + A: per-request mean over {repeats} colocated runs paired "
-                  f"against the per-request mean over {repeats + 1} standalone runs",
+        "design": f"interleaved A/B x{repeats} + A: per-request median over {repeats} colocated runs paired "
+                  f"against the per-request median over {repeats + 1} standalone runs (reference pairing, "
+                  f"metrics.cpp:49-65, on those per-request values)",
         "repeats": repeats,
         "ttft_delta_pct": ttft["mean_pct"], "ttft_delta_max_pct": ttft["max_pct"],
         "tpot_delta_pct": tpot["mean_pct"], "tpot_delta_max_pct": tpot["max_pct"], "pairs": ttft["pairs"],
+        "ttft_delta_runmean_pct": ttft_mean["mean_pct"], "tpot_delta_runmean_pct": tpot_mean["mean_pct"],
         "aa_noise_ttft_pct": aa_ttft["mean_pct"], "aa_noise_tpot_pct": aa_tpot["mean_pct"],
         "per_run_ttft_delta_pct": [paired_increase(base_ttft, c.ttft_us)["mean_pct"] for c in colos],
         "per_run_tpot_delta_pct": [paired_increase(base_tpot, c.tpot_us)["mean_pct"] for c in colos],
@@ -720,7 +743,8 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         "offline_ctas": offline_ctas or "default",
         "offline_gbs_harvested": colo.offline_bytes / colo.wall_s / 1e9,
         "offline_gemm": ({"shape": list(offline_gemm), "tflops_harvested": colo.offline_gemm_flop / colo.wall_s / 1e12,
-                          "tiles": colo.offline_gemm_tiles} if offline_gemm else None),
+                          "tiles": colo.offline_gemm_tiles, "ctas": offline_gemm_ctas or "one per SM"}
+                         if offline_gemm else None),
         "prefill_ms_median": {"standalone": _median([x for s in solos for x in s.prefill_us]) / 1e3,
                               "colocated": _median([x for c in colos for x in c.prefill_us]) / 1e3},
         "decode_iter_ms_median": {

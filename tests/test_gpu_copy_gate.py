@@ -210,6 +210,67 @@ def test_async_copy_overlaps_bookkeeping(oracle_c):
     pool.check_invariants()
 
 
+def test_pipelined_copies_back_to_back_reclaims(oracle_c):
+    """Two reclaim ops back to back with both copies in flight: the second decision rewrites
+    the report while the first (rate-bounded) copy still streams; each copy works from its own
+    snapshot, so both byte images match their own reports; waits complete FIFO."""
+    rng = random.Random(33)
+    pool, live = _pool_with_pages(rng, H=48, n_req=70)
+    _, _, n1 = pool.reclaim(4, 1000)
+    res1 = pool.last_reclaim()
+    buf1 = A.HostBuffer(n1 * pool.page_bytes)
+    pool.reclaim_copy_start(buf1.ptr, buf1.nbytes, A.copy_params(ctas=2, chunk_bytes=4096,
+                                                                   rate_bytes_per_s=3e8))
+    _, _, n2 = pool.reclaim(5, 1001)  # op 2 decides while op 1's bytes are in flight
+    res2 = pool.last_reclaim()
+    assert n2 > 0 and set(res2.handles).isdisjoint(res1.handles)
+    buf2 = A.HostBuffer(n2 * pool.page_bytes)
+    pool.reclaim_copy_start(buf2.ptr, buf2.nbytes, A.copy_params(ctas=4, chunk_bytes=8192))
+    with pytest.raises(A.LogicError):  # a third copy would exceed the ring
+        pool.reclaim_copy_start(buf2.ptr, buf2.nbytes)
+    with pytest.raises(A.LogicError):  # the synchronous form needs an idle ring
+        pool.reclaim_copy(buf2.ptr, buf2.nbytes)
+    st1 = pool.reclaim_copy_wait()
+    st2 = pool.reclaim_copy_wait()
+    assert (st1.bytes, st2.bytes) == (n1 * pool.page_bytes, n2 * pool.page_bytes)
+    assert np.array_equal(buf1.view(), _expected_images(oracle_c, res1, pool.page_bytes))
+    assert np.array_equal(buf2.view(), _expected_images(oracle_c, res2, pool.page_bytes))
+    with pytest.raises(A.LogicError):
+        pool.reclaim_copy_wait()
+    pool.check_invariants()
+
+
+def test_pipelined_copies_per_request_page_sizes(oracle_c):
+    """The ring also snapshots the variable-size layout (weight pages of a whole slot next to
+    KV pages): op 2's report (other sizes, other offsets) cannot leak into op 1's copy."""
+    rng = random.Random(8)
+    slot, page = 65536, 49152
+    pool = A.DevicePool(32, 8, 16, slot_bytes=slot, page_bytes=page)
+    weights = {3_000_000 + i: 9 for i in range(4)}
+    for w, n in weights.items():
+        assert pool.offline_reserve(w, n, 0)
+    kv = [r for r in range(60) if pool.offline_reserve(r, rng.randint(1, 6), 1)]
+    sizes = {w: slot for w in weights}
+    pool.set_page_bytes(sizes)
+    pool.fill_pages()
+    pool.set_costs({**{w: rng.randint(1, 10**6) for w in weights}, **{r: rng.randint(1, 100) for r in kv}})
+    ids1 = sorted(set(pool.handles_of_request(3_000_000)) | set(pool.handles_of_request(kv[0])))
+    res1 = pool.apply_reclaim(ids1, 10)
+    tot1, _ = pool.last_copy_layout()
+    buf1 = A.HostBuffer(tot1)
+    pool.reclaim_copy_start(buf1.ptr, buf1.nbytes, A.copy_params(ctas=2, chunk_bytes=8192,
+                                                                   rate_bytes_per_s=3e8))
+    pool.reclaim(6, 11)
+    res2 = pool.last_reclaim()
+    tot2, _ = pool.last_copy_layout()
+    buf2 = A.HostBuffer(max(tot2, 16))
+    pool.reclaim_copy_start(buf2.ptr, buf2.nbytes, A.copy_params(ctas=3, chunk_bytes=16384))
+    assert pool.reclaim_copy_wait().bytes == tot1
+    assert pool.reclaim_copy_wait().bytes == tot2
+    assert np.array_equal(buf1.view(), _expected_images_var(oracle_c, res1, sizes, page))
+    assert np.array_equal(buf2.view()[:tot2], _expected_images_var(oracle_c, res2, sizes, page))
+
+
 # ------------------------------------------------------------------- weight pages (C3)
 
 @pytest.mark.parametrize("slot,page,n_w", [(16384, 12288, 21), (1 << 20, 917504, 48)])

@@ -104,12 +104,17 @@ def test_gemm_quiesce_is_one_tile(mode):
     c = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
     gate = A.Gate(0)
     gs = torch.cuda.ExternalStream(gate.stream)
+    total = (m // (128 * mode)) * (n // 256)
     waits = []
     for gen in range(1, 21):
         gate.reset_work()
         side = torch.cuda.Stream()
         gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, stream=side.cuda_stream, mode=mode)
-        time.sleep(0.0003)
+        # raise once the kernel is running (a raise that lands before the launch's "gate open"
+        # wait, or after the last tile, preempts nothing and is not a quiesce sample)
+        deadline = time.perf_counter() + 0.5
+        while gate.read().tiles_claimed < 300 and time.perf_counter() < deadline:
+            pass
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(gs)
         gate.raise_(gen)
@@ -117,10 +122,14 @@ def test_gemm_quiesce_is_one_tile(mode):
         e1.record(gs)
         gate.release(gen)
         torch.cuda.synchronize()
-        waits.append(e0.elapsed_time(e1) * 1e3)
-        assert gate.read().tiles_done < (m // (128 * mode)) * (n // 256)  # it really was preempted
+        s = gate.read()
+        assert s.live_ctas == 0
+        assert s.tiles_done == min(s.tiles_claimed, total) <= total  # every claimed tile finished once
+        if 0 < s.tiles_done < total:
+            waits.append(e0.elapsed_time(e1) * 1e3)
+    assert len(waits) >= 10, waits  # most raises really preempted the GEMM mid-run
     waits.sort()
-    # one 128x256x3584 tile is ~0.23 GFLOP (~15 us on one SM's tensor cores)
+    # one 256x256 (pair) / 128x256 tile x 3584 is ~0.23-0.47 GFLOP (~15-30 us on its SMs)
     assert waits[len(waits) // 2] < 100.0, waits
 
 

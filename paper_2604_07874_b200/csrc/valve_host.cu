@@ -127,6 +127,7 @@ struct valve_pool {
   int last_custom = 0;          // some evicted request has its own page size
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaStream_t copy_stream = nullptr;  // reclaim copies overlap pool bookkeeping
+  cudaStream_t plan_stream = nullptr;  // report snapshots for queued copies (not behind a running copy)
   cudaEvent_t ev_report = nullptr;
   unsigned long long* d_copyctr = nullptr;  // restore / copy-engine counters (pool stream)
   // Reclaim copies in flight (FIFO ring).  Each copy first snapshots the report it needs (the
@@ -216,6 +217,7 @@ struct valve_pool {
         if (e) cudaEventDestroy(e);
     if (copy_stream) cudaStreamSynchronize(copy_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (plan_stream) cudaStreamDestroy(plan_stream);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -262,6 +264,7 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   ck(cudaEventCreate(&p->ev1), "cudaEventCreate");
   ck(cudaEventCreateWithFlags(&p->ev_report, cudaEventDisableTiming), "cudaEventCreate");
   ck(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaStreamCreateWithFlags(&p->plan_stream, cudaStreamNonBlocking), "cudaStreamCreate");
   const int H = p->H, S = p->S, R = p->R;
   const int64_t HS = (int64_t)H * S;
   PoolDev& d = p->d;
@@ -794,16 +797,19 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
     A.t_last = S.ctr + 2;
     // the copy runs on its own stream after the report exists and works from its own snapshot
     // of it; bookkeeping and the next decision proceed on the pool stream meanwhile
+    // the snapshot runs on the plan stream, so a copy queued behind a running one does not hold
+    // the next decision back; the slot is free (its previous copy completed: ring FIFO + wait)
     ck(cudaEventRecord(p->ev_report, p->stream), "event");
-    ck(cudaStreamWaitEvent(p->copy_stream, p->ev_report, 0), "event wait");
+    ck(cudaStreamWaitEvent(p->plan_stream, p->ev_report, 0), "event wait");
     const cudaMemcpyKind d2d = cudaMemcpyDeviceToDevice;
-    if (n_pages) ck(cudaMemcpyAsync(S.phys, p->d.res_phys, (size_t)n_pages * 4, d2d, p->copy_stream), "snapshot");
+    if (n_pages) ck(cudaMemcpyAsync(S.phys, p->d.res_phys, (size_t)n_pages * 4, d2d, p->plan_stream), "snapshot");
     if (custom && n_ev) {
-      ck(cudaMemcpyAsync(S.inv_off, p->d.res_inv_off, (size_t)(n_ev + 1) * 4, d2d, p->copy_stream), "snapshot");
-      ck(cudaMemcpyAsync(S.ev_pbytes, p->d.res_ev_pbytes, (size_t)n_ev * 8, d2d, p->copy_stream), "snapshot");
-      ck(cudaMemcpyAsync(S.ev_base, p->d.res_ev_base, (size_t)(n_ev + 1) * 8, d2d, p->copy_stream), "snapshot");
+      ck(cudaMemcpyAsync(S.inv_off, p->d.res_inv_off, (size_t)(n_ev + 1) * 4, d2d, p->plan_stream), "snapshot");
+      ck(cudaMemcpyAsync(S.ev_pbytes, p->d.res_ev_pbytes, (size_t)n_ev * 8, d2d, p->plan_stream), "snapshot");
+      ck(cudaMemcpyAsync(S.ev_base, p->d.res_ev_base, (size_t)(n_ev + 1) * 8, d2d, p->plan_stream), "snapshot");
     }
-    ck(cudaEventRecord(S.ev_plan, p->copy_stream), "event");
+    ck(cudaEventRecord(S.ev_plan, p->plan_stream), "event");
+    ck(cudaStreamWaitEvent(p->copy_stream, S.ev_plan, 0), "event wait");
     ck(cudaMemsetAsync(S.ctr, 0, 24, p->copy_stream), "memset");
     if (custom) {  // per-request page sizes: chunk prefix over the evicted requests first
       A.ev_pbytes = S.ev_pbytes;

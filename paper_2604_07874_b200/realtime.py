@@ -227,6 +227,7 @@ class RunResult:
     mech_ttft_us: Dict[int, float] = field(default_factory=dict)
     mech_tpot_us: Dict[int, float] = field(default_factory=dict)
     log: EventLog = field(default_factory=EventLog)
+    plan: list = field(default_factory=list)  # the action sequence this run executed
 
 
 class Colocation:
@@ -372,14 +373,27 @@ class Colocation:
             P.set_costs({r: self._off_cost[r] for r in self._off_live})
 
     # ------------------------------------------------------------------------ main loop
-    def run(self, trace: List[OnlineReq], offline_reqs=(), horizon_s: float = 30.0) -> RunResult:
+    def run(self, trace: List[OnlineReq], offline_reqs=(), horizon_s: float = 30.0,
+            plan: Optional[list] = None) -> RunResult:
+        """plan=None: the serving loop schedules (FIFO prefill-first, whole-batch decode) and the
+        result records, per prefill, (request, decode iterations completed before it) in res.plan.
+        plan=<a recorded list>: prefills happen in the recorded order at the recorded decode
+        counts (never before the request's arrival; if it arrives later than in the recording the
+        prefill goes at the first boundary after it), so a paired run differs from its baseline
+        only in how long each step takes -- not in which decode iterations a prefill happened to
+        fall between (a wall-clock loop flips that on microseconds of jitter, moving a request's
+        TPOT by several ms)."""
         m = self.model
         self.res = RunResult({}, {}, 0.0)
+        pi = 0  # next planned prefill
+        n_decodes = 0  # decode iterations so far (the replay clock)
+        by_rid = {}
         self._evicted, self._off_live, self._off_req_pages, self._off_cost = [], {}, {}, {}
         self._off_pages = 0
         self._harvest = 0
         self._gemm_harvest = 0
         reqs = [OnlineReq(r.rid, r.arrival_us, r.prompt, r.output) for r in trace]
+        by_rid = {r.rid: r for r in reqs}
         log = self.res.log
         log.add(0, "run_meta", scenario="realtime_spike", preset="valve" if self.colocated else "standalone",
                 seed=0, gpus=1, horizon_us=int(horizon_s * 1e6), online_fingerprint=trace_fingerprint(trace),
@@ -424,14 +438,31 @@ class Colocation:
                         prompt_tokens=r.prompt, output_tokens=r.output)
                 queue.append(r)
                 nxt += 1
-            if not queue and not decoding:
+            act = None  # next action: ("prefill", rid) / ("decode", batch size); None = idle
+            if plan is None:
+                if queue:
+                    act = ("prefill", queue[0].rid)
+                elif decoding:
+                    act = ("decode", len(decoding))
+                finished = act is None and nxt >= len(reqs)
+            else:
+                # prefill the next planned request at the decode count it had in the recording
+                # (or at the first boundary after its arrival if this run got there earlier)
+                finished = pi >= len(plan) and not decoding
+                if pi < len(plan):
+                    rid, k = plan[pi]
+                    if by_rid[rid].arrival_us <= now and (n_decodes >= k or not decoding):
+                        act = ("prefill", rid)
+                if act is None and decoding:
+                    act = ("decode", len(decoding))
+            if act is None:
                 if busy:  # idle edge (sim.cpp:371-380)
                     busy = False
                     log.add(now, "busy", gpu=0, **{"class": "online"}, start_us=busy_since, end_us=now)
                     if self.colocated:
                         self.channel.note_all_idle(now)
                         self._readmit_offline(now)
-                if nxt >= len(reqs):
+                if finished:
                     break
                 if self.colocated and self.channel.offline_compute_allowed():
                     # the offline engine's next iteration: a pass over its KV finished -> relaunch
@@ -441,6 +472,11 @@ class Colocation:
                         self._launch_gemm()
                 time.sleep(50e-6)
                 continue
+            if act[0] == "prefill":
+                self.res.plan.append((act[1], n_decodes))
+                pi += 1
+            else:
+                n_decodes += 1
             if not busy:  # busy edge: raise + wait for the offline CTAs to retire (sim.cpp:362-369)
                 busy = True
                 busy_since = now
@@ -454,8 +490,9 @@ class Colocation:
                     e1.record(self.online_stream)
                     pending_wait = (e0, e1)  # charged to the request this edge admits
                     self.res.disables = self.channel.disables_issued()
-            if queue:  # prefill the queue head
-                r = queue.pop(0)
+            if act[0] == "prefill":  # prefill the queue head (or the planned request)
+                r = by_rid[act[1]]
+                queue.remove(r)
                 need = -(-r.prompt // self.page_tokens)
                 if self.colocated:
                     ta = time.perf_counter()
@@ -646,7 +683,7 @@ def _med_runs(dicts):
 
 def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, handles=64, seed=2604,
                    output=(8, 12), prompt=(2500, 3500), layers=32, device=0, offline_ctas=0, repeats=1,
-                   offline_gemm=None, offline_gemm_ctas: int = 0,
+                   offline_gemm=None, offline_gemm_ctas: int = 0, replay: bool = True,
                    log_dir: Optional[str] = None):
     """Paired standalone vs colocated run of one online trace (default: the pair_06 shape --
     spike base 0.3/s, 6/s for 1 s every 8 s, prompt 2500-3500, output 8-12 -- so the online
@@ -665,11 +702,18 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
     model = OnlineModel(ModelShape(layers=layers), dev)
     trace = spike_trace(seed, horizon, base, spike, period, width, prompt=prompt, output=output)
     warm_shapes(model, trace)
+    # replay=True: an untimed standalone run records the serving loop's action sequence, and
+    # every measured run (standalone and colocated) replays it -- the pairing then compares the
+    # same work, action by action (see Colocation.run)
+    plan = None
+    if replay:  # the second of two live runs (the first one still pays first-use costs)
+        for _ in range(2):
+            plan = Colocation(model, None, None).run(trace, horizon_s=horizon + 30).plan
     solos, colos = [], []
     clocks = {"standalone": [], "colocated": []}
     for i in range(repeats):
         with _Clocks(device) as ck:
-            solos.append(Colocation(model, None, None).run(trace, horizon_s=horizon + 30))
+            solos.append(Colocation(model, None, None).run(trace, horizon_s=horizon + 30, plan=plan))
         clocks["standalone"].append(ck.summary())
         pool = A.DevicePool(handles, 64, 16, device=device, slot_bytes=2 << 20, page_bytes=917504,
                             max_requests=4096, max_pages_per_request=1024)
@@ -677,7 +721,7 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         colo_rt = Colocation(model, pool, gate, offline_ctas=offline_ctas, offline_gemm=offline_gemm,
                              offline_gemm_ctas=offline_gemm_ctas)
         with _Clocks(device) as ck:
-            colos.append(colo_rt.run(trace, offline_population(seed, 4 * handles), horizon_s=horizon + 30))
+            colos.append(colo_rt.run(trace, offline_population(seed, 4 * handles), horizon_s=horizon + 30, plan=plan))
         clocks["colocated"].append(ck.summary())
         del pool, gate, colo_rt
         import gc
@@ -685,7 +729,7 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         gc.collect()  # the channel's ctypes hooks close over the runtime: break the cycle now
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
-    solos.append(Colocation(model, None, None).run(trace, horizon_s=horizon + 30))
+    solos.append(Colocation(model, None, None).run(trace, horizon_s=horizon + 30, plan=plan))
     if log_dir:
         import os
 
@@ -718,6 +762,8 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         "trace": {"horizon_s": horizon, "online_requests": len(trace), "base_rate": base, "spike_rate": spike,
                   "period_s": period, "width_s": width, "prompt": list(prompt), "output": list(output),
                   "model": f"Llama-3-8B-shaped, {layers} layers, random init bf16"},
+        "schedule": ("replayed: every run places each prefill at the decode count recorded by an untimed "
+                     f"standalone run ({len(plan)} prefills)") if plan else "live (each run schedules on its own)",
         "design": f"interleaved A/B x{repeats} + A: per-request median over {repeats} colocated runs paired "
                   f"against the per-request median over {repeats + 1} standalone runs (reference pairing, "
                   f"metrics.cpp:49-65, on those per-request values)",

@@ -97,6 +97,17 @@ def test_gemm_preempt_resume_conserves_tiles(mode):
     assert torch.equal(c.view(torch.int16), c_ref.view(torch.int16))
 
 
+def _drain(what, ev, gate, limit_s=10.0):
+    """Wait for `ev` (an event or stream) with a deadline; a timeout fails with the gate state
+    instead of hanging the session."""
+    t0 = time.perf_counter()
+    while not ev.query():
+        if time.perf_counter() - t0 > limit_s:
+            s = gate.read()
+            pytest.fail(f"{what} did not complete: live_ctas={s.live_ctas} claimed={s.tiles_claimed} "
+                        f"done={s.tiles_done} closed={s.closed} quiesced_gen={s.quiesced_gen}")
+
+
 @pytest.mark.parametrize("mode", [1, 2])
 def test_gemm_quiesce_is_one_tile(mode):
     m, n, k = 8192, 18944, 3584  # Qwen2-7B gate/up projection over 8192 tokens: 4,736 tiles
@@ -105,10 +116,11 @@ def test_gemm_quiesce_is_one_tile(mode):
     gate = A.Gate(0)
     gs = torch.cuda.ExternalStream(gate.stream)
     total = (m // (128 * mode)) * (n // 256)
+    side = torch.cuda.Stream()  # one stream for the whole test (pool streams are recycled)
     waits = []
+    torch.cuda.synchronize()
     for gen in range(1, 21):
         gate.reset_work()
-        side = torch.cuda.Stream()
         gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, stream=side.cuda_stream, mode=mode)
         # raise once the kernel is running (a raise that lands before the launch's "gate open"
         # wait, or after the last tile, preempts nothing and is not a quiesce sample)
@@ -120,8 +132,9 @@ def test_gemm_quiesce_is_one_tile(mode):
         gate.raise_(gen)
         gate.wait_quiesced(gen)
         e1.record(gs)
+        _drain(f"quiesce wait (gen {gen})", e1, gate)
         gate.release(gen)
-        torch.cuda.synchronize()
+        _drain(f"gated GEMM launch (gen {gen})", side, gate)
         s = gate.read()
         assert s.live_ctas == 0
         assert s.tiles_done == min(s.tiles_claimed, total) <= total  # every claimed tile finished once

@@ -374,7 +374,7 @@ class Colocation:
 
     # ------------------------------------------------------------------------ main loop
     def run(self, trace: List[OnlineReq], offline_reqs=(), horizon_s: float = 30.0,
-            plan: Optional[list] = None) -> RunResult:
+            plan: Optional[list] = None, admit_margin_us: int = 0) -> RunResult:
         """plan=None: the serving loop schedules (FIFO prefill-first, whole-batch decode) and the
         result records, per prefill, (request, decode iterations completed before it) in res.plan.
         plan=<a recorded list>: prefills happen in the recorded order at the recorded decode
@@ -382,7 +382,9 @@ class Colocation:
         prefill goes at the first boundary after it), so a paired run differs from its baseline
         only in how long each step takes -- not in which decode iterations a prefill happened to
         fall between (a wall-clock loop flips that on microseconds of jitter, moving a request's
-        TPOT by several ms)."""
+        TPOT by several ms).  admit_margin_us (recording runs): while a batch is decoding, a
+        request is prefilled only at a boundary at least this long after its arrival, so a replay
+        whose clock runs a little ahead of the recording still finds it arrived."""
         m = self.model
         self.res = RunResult({}, {}, 0.0)
         pi = 0  # next planned prefill
@@ -440,7 +442,7 @@ class Colocation:
                 nxt += 1
             act = None  # next action: ("prefill", rid) / ("decode", batch size); None = idle
             if plan is None:
-                if queue:
+                if queue and (not decoding or queue[0].arrival_us <= now - admit_margin_us):
                     act = ("prefill", queue[0].rid)
                 elif decoding:
                     act = ("decode", len(decoding))
@@ -708,7 +710,7 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
     plan = None
     if replay:  # the second of two live runs (the first one still pays first-use costs)
         for _ in range(2):
-            plan = Colocation(model, None, None).run(trace, horizon_s=horizon + 30).plan
+            plan = Colocation(model, None, None).run(trace, horizon_s=horizon + 30, admit_margin_us=3000).plan
     solos, colos = [], []
     clocks = {"standalone": [], "colocated": []}
     for i in range(repeats):

@@ -55,7 +55,9 @@ def parse():
     ap.add_argument("--k", type=int, default=36)
     ap.add_argument("--handles", type=int, default=0)
     ap.add_argument("--preemptions", type=int, default=1000)
-    ap.add_argument("--copy-ctas", type=int, default=32)
+    ap.add_argument("--copy-ctas", type=int, default=8,
+                    help="copy CTAs: 8 already saturate the link (tools/copy_sweep.py); fewer CTAs keep fewer "
+                         "bytes queued on PCIe ahead of the next decision's small host-mapped writes")
     ap.add_argument("--copy-threads", type=int, default=512)
     ap.add_argument("--tma", type=int, default=0)
     ap.add_argument("--seed", type=int, default=2604)

@@ -240,7 +240,7 @@ class Colocation:
         self.model, self.pool, self.gate = model, pool, gate
         self.page_tokens = page_tokens
         self.tile_bytes = tile_bytes
-        self.offline_ctas = offline_ctas  # 0 = library default (2 CTAs of 8 warps per SM)
+        self.offline_ctas = offline_ctas  # 0 = library default (2 CTAs of 8 warps per SM); < 0 = no decode pass
         self.colocated = pool is not None
         self.online_stream = torch.cuda.current_stream()
         self.off_stream = torch.cuda.Stream()
@@ -300,6 +300,8 @@ class Colocation:
                                    m, n, k, ctas=self.gemm_ctas, stream=self.gemm_stream.cuda_stream, fresh=fresh)
 
     def _launch_decode(self):
+        if self.offline_ctas < 0:
+            return
         st = self.gate.read()
         total = self._offline_tiles_total()
         if total and st.tiles_claimed >= total:  # work list exhausted: start another pass
@@ -468,7 +470,7 @@ class Colocation:
                     break
                 if self.colocated and self.channel.offline_compute_allowed():
                     # the offline engine's next iteration: a pass over its KV finished -> relaunch
-                    if self.gate.read().live_ctas == 0:
+                    if self.offline_ctas >= 0 and self.gate.read().live_ctas == 0:
                         self._launch_decode()
                     if self.gemm_gate is not None and self.gemm_gate.read().live_ctas == 0:
                         self._launch_gemm()

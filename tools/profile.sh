@@ -7,7 +7,7 @@
 set -x
 mkdir -p gpurun_out
 make -C oracle >/dev/null
-ARGS="--steps 2 --warmup 1 --preemptions 5 --skip-realtime"
+ARGS="--steps 2 --warmup 1 --preemptions 5 --skip-realtime --skip-fanout"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py $ARGS --profile-mode > gpurun_out/launches_bench.log 2>&1
 for k in ${KERNELS:-k_reclaim_copy k_reclaim k_offline_decode k_offline_gemm k_restore_scatter k_apply k_offline_reserve}; do

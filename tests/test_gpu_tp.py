@@ -97,3 +97,47 @@ def test_tp_group_of_two_processes_shares_the_gate():
     # two processes on one GPU are time-sliced contexts (no MPS): latency here is not the TP
     # fan-out's (tools/tp_fanout.py measures it); only bound it loosely
     assert res[0]["quiesce_us"] < 50_000
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fanout_modes_quiesce_every_member_same_process(mode):
+    """Leader + 3 member gates in one process (each member runs its own gated decode pass):
+    one raise closes every member, one wait returns only when all of them retired (both ack-wait
+    forms: batched memops / helper streams), nothing is claimed while closed, and after the
+    release every member's pass resumes and completes each tile exactly once."""
+    import torch
+
+    from paper_2604_07874_b200 import api as A
+
+    pool = A.DevicePool(64, 16, 16, slot_bytes=1 << 20, page_bytes=917504)
+    for r in range(64):
+        pool.offline_reserve(r, 16, 0)
+    pool.fill_pages()
+    gates = [A.Gate(0) for _ in range(4)]
+    gates[0].set_fanout(mode)
+    gates[0].attach_peers(gates[1:])
+    streams = [torch.cuda.Stream() for _ in gates]
+    total = 64 * 16 * (-(-917504 // 16384))
+    for g, s in zip(gates, streams):
+        g.reset_work()
+        g.launch_offline(pool, None, None, 0, 0, None, ctas=8, stream=s.cuda_stream)
+    time.sleep(0.002)
+    gates[0].raise_(7)
+    gates[0].wait_quiesced(7)
+    torch.cuda.ExternalStream(gates[0].stream).synchronize()
+    st = [g.read() for g in gates]
+    assert all(s.closed == 1 and s.live_ctas == 0 and s.quiesced_gen == 7 for s in st), \
+        [(s.closed, s.live_ctas, s.quiesced_gen) for s in st]
+    assert all(s.tiles_done == s.tiles_claimed for s in st)  # claimed tiles all finished
+    time.sleep(0.005)
+    assert [g.read().tiles_claimed for g in gates] == [s.tiles_claimed for s in st]  # nothing claimed
+    gates[0].release(7)
+    torch.cuda.ExternalStream(gates[0].stream).synchronize()
+    assert all(g.read().closed == 0 for g in gates)
+    for g, s in zip(gates, streams):
+        g.launch_offline(pool, None, None, 0, 0, None, ctas=8, stream=s.cuda_stream)
+    for s in streams:
+        s.synchronize()
+    assert [g.read().tiles_done for g in gates] == [total] * 4  # every tile exactly once
+    with pytest.raises(A.InvalidArgument):
+        gates[0].set_fanout(5)

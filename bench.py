@@ -531,6 +531,9 @@ def run_valve(args, rank, world, dist):
 
     # ------------------------------------------------ copy-engine alternative (same report)
     pool.reclaim(args.k, t + 5, 0)
+    ce_res = pool.last_reclaim()
+    flat = [p for r in ce_res.evicted_requests for p in ce_res.physical_pages[r]]
+    ce_runs = sum(1 for i, p in enumerate(flat) if i == 0 or p != flat[i - 1] + 1)  # 2D transfers
     ce = pool.reclaim_copy(host.ptr, host.nbytes, engine="ce")
     ce_gbs = ce.bytes / (ce.kernel_ms * 1e-3) / 1e9
     restore(pool.last_reclaim().evicted_requests)
@@ -674,6 +677,7 @@ def run_valve(args, rank, world, dist):
         "decision_us_mean": round(statistics.mean(stats["reclaim_ms"]) * 1e3, 1),
         "copy_engine_alt_gbs": round(ce_gbs, 2),
         "copy_engine_alt_frac": round(ce_gbs / peak, 4),
+        "copy_engine_alt_transfers": ce_runs,
         "copy_note": "SM-issued sysmem stores leave as 128 B PCIe TLPs vs 256 B for the copy engines: "
                      "the SM kernel's ceiling is (128/152)/(256/280) = 92.1% of the CE-measured peak",
         "step_quiesce_us_mean": round(statistics.mean(stats["quiesce_us"]), 1),

@@ -980,25 +980,33 @@ int valve_pool_reclaim_copy_ce(valve_pool* p, void* host_dst, int64_t dst_bytes,
             offs[j] = (size_t)(base[e] + (int64_t)(j - io[e]) * pb[e]);
           }
     }
-    // one batched copy-engine submission (CUDA >= 12.8); per-page copies if unsupported
-    std::vector<void*> dsts(phys.size()), srcs(phys.size());
+    // Pages that sit in consecutive physical slots and land back to back in the destination form
+    // a run: one 2D copy-engine transfer (source pitch = slot, destination pitch = page) instead
+    // of one transfer per page, so the per-copy setup no longer shows against the link rate.
+    struct Run { size_t first, n; };
+    std::vector<Run> runs;
     for (size_t i = 0; i < phys.size(); ++i) {
-      dsts[i] = static_cast<uint8_t*>(host_dst) + offs[i];
-      srcs[i] = p->d.pages + (int64_t)phys[i] * p->d.slot_bytes;
+      if (!runs.empty()) {
+        Run& r = runs.back();
+        const size_t j = r.first + r.n - 1;
+        if (phys[i] == phys[j] + 1 && sizes[i] == sizes[j] && offs[i] == offs[j] + sizes[j]) {
+          ++r.n;
+          continue;
+        }
+      }
+      runs.push_back({i, 1});
     }
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t attr_idx = 0, fail_idx = 0;
     ck(cudaEventRecord(p->ev0, p->stream), "event");
-    bool batched = false;
-    if (!phys.empty()) {
-      batched = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), phys.size(), &attr, &attr_idx,
-                                     1, &fail_idx, p->stream) == cudaSuccess;
-      if (!batched) cudaGetLastError();
+    for (const Run& r : runs) {
+      uint8_t* dst = static_cast<uint8_t*>(host_dst) + offs[r.first];
+      const uint8_t* src = p->d.pages + (int64_t)phys[r.first] * p->d.slot_bytes;
+      const size_t w = sizes[r.first];
+      if (r.n == 1 || w == (size_t)p->d.slot_bytes)
+        ck(cudaMemcpyAsync(dst, src, w * r.n, cudaMemcpyDeviceToHost, p->stream), "cudaMemcpyAsync");
+      else
+        ck(cudaMemcpy2DAsync(dst, w, src, (size_t)p->d.slot_bytes, w, r.n, cudaMemcpyDeviceToHost, p->stream),
+           "cudaMemcpy2DAsync");
     }
-    if (!batched)
-      for (size_t i = 0; i < phys.size(); ++i)
-        ck(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDeviceToHost, p->stream), "cudaMemcpyAsync");
     ck(cudaEventRecord(p->ev1, p->stream), "event");
     ck(cudaStreamSynchronize(p->stream), "reclaim_copy_ce");
     if (st) {

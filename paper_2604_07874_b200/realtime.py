@@ -428,6 +428,11 @@ class Colocation:
         pending_wait = None
         wait_events = []
         torch.cuda.synchronize()
+        import gc
+
+        gc.collect()
+        gc_was = gc.isenabled()
+        gc.disable()  # a generation-2 collection in the loop is a 10-100 ms stall on either arm
         t0 = time.perf_counter()
         now_us = lambda: int((time.perf_counter() - t0) * 1e6)  # noqa: E731
         while True:
@@ -559,6 +564,8 @@ class Colocation:
                         first_token_us=r.emits[0], last_token_us=r.emits[-1], digest="0x0000000000000000")
         self.online_stream.synchronize()  # never a device-wide sync: a gated launch may be queued
         self.res.wall_s = time.perf_counter() - t0
+        if gc_was:
+            gc.enable()
         if busy:
             log.add(now_us(), "busy", gpu=0, **{"class": "online"}, start_us=busy_since, end_us=now_us())
         for (t_adm, _), (rid, (e0, e1)) in zip(preempt_rids, wait_events):
@@ -617,7 +624,7 @@ def warm_shapes(model: OnlineModel, trace: List[OnlineReq]):
 
 
 class _Clocks:
-    """nvidia-smi SM clock / power samples (100 ms) over one run -- evidence for clock effects of
+    """nvidia-smi SM clock / power samples (500 ms) over one run -- evidence for clock effects of
     the offline tenant (a tensor-heavy tenant in the gaps can push the GPU into its power cap)."""
 
     def __init__(self, device):
@@ -630,7 +637,7 @@ class _Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,power.draw",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "500"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:

@@ -775,6 +775,10 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
                   "model": f"Llama-3-8B-shaped, {layers} layers, random init bf16"},
         "schedule": ("replayed: every run places each prefill at the decode count recorded by an untimed "
                      f"standalone run ({len(plan)} prefills)") if plan else "live (each run schedules on its own)",
+        # prefills a run executed at another decode count than the plan's (arrival later than the
+        # recording's boundary); 0 everywhere = both arms ran exactly the same schedule
+        "plan_deviations": ({"standalone": [_deviations(plan, r.plan) for r in solos],
+                             "colocated": [_deviations(plan, r.plan) for r in colos]} if plan else None),
         "design": f"interleaved A/B x{repeats} + A: per-request median over {repeats} colocated runs paired "
                   f"against the per-request median over {repeats + 1} standalone runs (reference pairing, "
                   f"metrics.cpp:49-65, on those per-request values)",
@@ -817,6 +821,11 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     return out
+
+
+def _deviations(plan, executed):
+    want = {rid: k for rid, k in plan}
+    return sum(1 for rid, k in executed if want.get(rid) != k)
 
 
 def _attributable(mech, base, per):

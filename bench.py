@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--skip-fanout", action="store_true", help="skip the same-device TP fan-out sweep")
     ap.add_argument("--rt-horizon", type=float, default=24.0, help="online trace length (s)")
     ap.add_argument("--rt-repeats", type=int, default=3, help="colocated runs (interleaved with standalone)")
+    ap.add_argument("--rt-decode-ctas", type=int, default=16,
+                    help="offline KV decode-pass CTAs in the real-time run (-1 = none, 0 = library default)")
+    ap.add_argument("--rt-gemm-ctas", type=int, default=64, help="offline GEMM CTAs in the real-time run (0 = all SMs)")
     ap.add_argument("--rt-gemm", default="2048,37888,3584",
                     help="m,n,k of the offline tenant's gated tcgen05 GEMM (Qwen2-7B gate/up); '' = decode pass only")
     ap.add_argument("--profile-mode", action="store_true",
@@ -633,10 +636,14 @@ def run_valve(args, rank, world, dist):
         torch.cuda.empty_cache()
         from paper_2604_07874_b200 import realtime as RT
 
-        # offline harvest at one 8-warp CTA per SM (~3.7 TB/s of HBM reads in the gaps)
-        rt = RT.measure_deltas(horizon=args.rt_horizon, device=gpu, seed=args.seed + rank, offline_ctas=148,
-                               repeats=args.rt_repeats,
+        # power-headroom tenant: the KV decode pass on 16 CTAs + the gated GEMM on 64 SMs keeps the
+        # board below its power cap, so the online tenant starts each busy period at full clock
+        # (an all-SM GEMM tenant holds ~985 W / ~1,680 MHz and costs the first prefill ~5 %;
+        # tools/realtime_sweep.py)
+        rt = RT.measure_deltas(horizon=args.rt_horizon, device=gpu, seed=args.seed + rank,
+                               offline_ctas=args.rt_decode_ctas, repeats=args.rt_repeats,
                                offline_gemm=tuple(int(x) for x in args.rt_gemm.split(",")) if args.rt_gemm else None,
+                               offline_gemm_ctas=args.rt_gemm_ctas,
                                log_dir=os.path.join(ROOT, "gpurun_out", "realtime_logs"))
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "r1_copy_traffic.json")))

@@ -800,11 +800,14 @@ class DevicePool(MemoryPool):
         return st
 
     def reclaim_copy_start(self, host_ptr: int, nbytes: int, params: Optional[CopyParams] = None):
-        """Start the gather copy asynchronously (overlaps later bookkeeping calls)."""
+        """Start the gather copy of the last reclaim's report asynchronously.  The copy works from
+        its own snapshot of the report, so bookkeeping calls and the next reclaim / apply_reclaim
+        overlap it; up to two copies may be in flight (valve_pool_reclaim_copy_start)."""
         self._b.check(self._b.lib.valve_pool_reclaim_copy_start(
             self._h, C.c_void_p(host_ptr), int(nbytes), C.byref(params) if params is not None else None))
 
     def reclaim_copy_wait(self) -> CopyStats:
+        """Complete the oldest copy in flight (FIFO) and return its stats."""
         st = CopyStats()
         self._b.check(self._b.lib.valve_pool_reclaim_copy_wait(self._h, C.byref(st)))
         return st

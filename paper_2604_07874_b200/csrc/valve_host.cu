@@ -205,7 +205,9 @@ struct valve_pool {
   }
 
   ~valve_pool() {
-    if (stream) cudaStreamSynchronize(stream);
+    // drain in-flight copies (and their report snapshots) before their buffers go away
+    for (cudaStream_t s : {plan_stream, copy_stream, stream})
+      if (s) cudaStreamSynchronize(s);
     for (void* p : dev_allocs) cudaFree(p);
     if (d.pages) cudaFree(d.pages);
     if (mirror) cudaFreeHost(mirror);
@@ -215,7 +217,6 @@ struct valve_pool {
     for (CopySlot& c : cs)
       for (cudaEvent_t e : {c.ev0, c.ev1, c.ev_plan})
         if (e) cudaEventDestroy(e);
-    if (copy_stream) cudaStreamSynchronize(copy_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (plan_stream) cudaStreamDestroy(plan_stream);
     if (stream) cudaStreamDestroy(stream);

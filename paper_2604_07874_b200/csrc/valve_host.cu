@@ -132,7 +132,7 @@ struct valve_pool {
   unsigned long long* d_copyctr = nullptr;  // restore / copy-engine counters (pool stream)
   // Reclaim copies in flight (FIFO ring).  Each copy first snapshots the report it needs (the
   // physical page list, plus the byte layout for per-request page sizes) into its own slot on
-  // the copy stream, so the next decision may rewrite the report while the bytes are still
+  // the plan stream, so the next decision may rewrite the report while the bytes are still
   // crossing the link: back-to-back reclaim ops keep the host link busy.
   struct CopySlot {
     int* phys = nullptr;

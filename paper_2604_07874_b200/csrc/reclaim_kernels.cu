@@ -20,20 +20,23 @@ constexpr int kSmemHandles = 2048;   // greedy in shared memory up to this many 
 constexpr int kSmemListings = 4096;  // ... and this many (handle, request) listings
 constexpr int kSmemTuples = 8192;    // invalidation report sorted in shared memory
 // dynamic shared memory of k_reclaim / k_apply / k_select_instance (host sets the attribute):
-// greedy 2048*(8+4+4+1) + 4096*(8+4+4+4+4+4) + 4 = 149,508 B; apply sort 8192*12 = 98,304 B
-static_assert(kSmemHandles * 17 + kSmemListings * 28 + 64 <= 160 * 1024, "greedy smem");
+// greedy 2048*(8+4+4+1+4) + 4096*(8+4+4+4+4+4) + 4 = 157,700 B; apply sort 8192*12 = 98,304 B
+static_assert(kSmemHandles * 21 + kSmemListings * 28 + 64 <= 160 * 1024, "greedy smem");
 static_assert(kSmemTuples * 12 <= 160 * 1024, "sort smem");
 
 __device__ long long g_greedy_cycles[2];  // diagnostics: argmin / update cycles of the last run
 __device__ long long g_apply_ns[6];       // diagnostics: apply_core phase stamps of the last run
 
-// Ref lists of instance handle i: CSR (off) or fixed stride with counts (cnt).
+// Ref lists of instance handle i: CSR (off) or fixed stride with counts (cnt), the stride slot
+// being i itself or map[i] (the fused reclaim lays rows out by handle id: map = instance ids).
 struct Refs {
   const int* off;
   const int* cnt;
   int stride;
-  __device__ __forceinline__ int begin(int i) const { return cnt ? i * stride : off[i]; }
-  __device__ __forceinline__ int end(int i) const { return cnt ? i * stride + cnt[i] : off[i + 1]; }
+  const int* map = nullptr;
+  __device__ __forceinline__ int slot(int i) const { return map ? map[i] : i; }
+  __device__ __forceinline__ int begin(int i) const { return cnt ? slot(i) * stride : off[i]; }
+  __device__ __forceinline__ int end(int i) const { return cnt ? slot(i) * stride + cnt[slot(i)] : off[i + 1]; }
 };
 
 // Reverse index request -> handle indices (one entry per listing, duplicates kept), and
@@ -189,6 +192,60 @@ __device__ void greedy_block(int n, const int* hid, Refs R, const int* rref, con
   if (t == 0) g_greedy_cycles[0] = c_arg, g_greedy_cycles[1] = c_upd;
 }
 
+// Packed-key rounds.  The caller guarantees hid[] ascending (index order = id order), every
+// cost >= 0 and every initial marginal < 2^(32 - idbits): the lexicographic (marginal, id) key
+// then packs into one u32, key = (marginal << idbits) | index, and stays exact as marginals only
+// shrink.  Keys live in shared memory: each argmin level is one redux.sync.min, and the winner's
+// evictions subtract (cost << idbits) straight from the listed handles' keys with u32 atomics
+// (no per-owner fold pass).  Taken handles are masked by their owner's `live` bits.
+__device__ void greedy_block_packed(int n, const int* hid, Refs R, const int* rref, const int64_t* cost,
+                                    int k, const int64_t* marg0, unsigned* skey, int* ev, const int* qoff,
+                                    const int* qh, int* out, int idbits) {
+  constexpr int NW = kGreedyThreads / 32;
+  __shared__ unsigned w_key[NW];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const unsigned idmask = (1u << idbits) - 1u;
+  unsigned live = 0;
+#pragma unroll
+  for (int j = 0; j < kGreedyOwn; ++j) {
+    const int i = t + j * kGreedyThreads;
+    if (i < n) {
+      live |= 1u << j;
+      skey[i] = ((unsigned)marg0[i] << idbits) | (unsigned)i;
+    }
+  }
+  greedy_bar();
+  long long c_arg = 0, c_upd = 0;
+  for (int round = 0; round < k; ++round) {
+    const long long c0 = clock64();
+    unsigned v = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < kGreedyOwn; ++j)
+      if ((live >> j) & 1u) v = min(v, skey[t + j * kGreedyThreads]);
+    v = __reduce_min_sync(kFull, v);
+    if (lane == 0) w_key[wid] = v;
+    greedy_bar();
+    v = __reduce_min_sync(kFull, lane < NW ? w_key[lane] : 0xFFFFFFFFu);
+    const int best = (int)(v & idmask);
+    const long long c1 = clock64();
+    c_arg += c1 - c0;
+#pragma unroll
+    for (int j = 0; j < kGreedyOwn; ++j)
+      if (best == t + j * kGreedyThreads) live &= ~(1u << j);
+    if (t == 0) out[round] = hid[best];
+    for (int e = R.begin(best) + t; e < R.end(best); e += kGreedyThreads) {
+      const int r = rref[e];
+      if (atomicExch(&ev[r], 1) == 0) {
+        const unsigned dec = (unsigned)cost[r] << idbits;
+        for (int q = qoff[r]; q < qoff[r + 1]; ++q) atomicSub(&skey[qh[q]], dec);
+      }
+    }
+    greedy_bar();
+    c_upd += clock64() - c1;
+  }
+  if (t == 0) g_greedy_cycles[0] = c_arg, g_greedy_cycles[1] = c_upd;
+}
+
 // Same rounds CTA-wide over global arrays (instances larger than shared memory).
 __device__ void greedy_cta(int n, const int* hid, Refs R, const int* rref, const int64_t* cost,
                            int k, int64_t* marg, int* taken, int* ev, const int* qoff, const int* qh,
@@ -309,8 +366,21 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
       marg[i] = s;
     }
     __syncthreads();
+    // packed-key rounds when ids ascend, costs are >= 0 and the marginals fit the key
+    int idbits = 1;
+    while ((1 << idbits) < n) ++idbits;
+    const int64_t lim = (int64_t)1 << (32 - idbits);
+    int bad = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      bad |= (marg[i] >= lim) | (i + 1 < n && hid[i] >= hid[i + 1]);
+    for (int d = threadIdx.x; d < m2; d += blockDim.x) bad |= cost2[d] < 0;
+    const bool packed = __syncthreads_or(bad) == 0;
     const Refs Rs{roff, nullptr, 0};
-    if (threadIdx.x < kGreedyThreads) greedy_block(n, hid, Rs, rr, cost2, k, marg, ev2, qoff2, qh2, out);
+    unsigned* skey = reinterpret_cast<unsigned*>(taken + kSmemHandles);
+    if (threadIdx.x < kGreedyThreads) {
+      if (packed) greedy_block_packed(n, hid, Rs, rr, cost2, k, marg, skey, ev2, qoff2, qh2, out, idbits);
+      else greedy_block(n, hid, Rs, rr, cost2, k, marg, ev2, qoff2, qh2, out);
+    }
     __syncthreads();
   } else {
     build_instance_index(n, R, rref, m, cost, marg_g, qoff, qcnt, qh, ev);
@@ -649,14 +719,25 @@ __global__ void __launch_bounds__(kNT) k_apply(PoolDev P, const int* ids, int k,
   publish(P);
 }
 
-// Fused reclaim (sim.cpp:936-942 in one launch): build the instance from the live slots
-// (the snapshot), select k handles with the row costs, apply.
+// Fused reclaim, part 1 (grid over the handles, warp per handle): the distinct resident rows
+// of every offline handle, laid out by handle id (s_rref + h*S, s_cnt[h]).  Spread over the
+// whole GPU this is ~2 us; inside the single-CTA part 2 it was 32 warps x ~30 handles each.
+__global__ void __launch_bounds__(256) k_reclaim_rows(PoolDev P) {
+  const int lane = threadIdx.x & 31;
+  const int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.mirror->r[3] = (int64_t)globaltimer_ns();  // phase stamps
+  if (h >= P.H || P.hstate[h] != kOffline) return;
+  const int nc = (P.S + 31) >> 5;
+  int cnt = 0;
+  VALVE_DISPATCH_NC(nc, cnt = warp_distinct_rows<NC>(P, h, P.s_rref + (int64_t)h * P.S));
+  if (lane == 0) P.s_cnt[h] = cnt;
+}
+
+// Fused reclaim, part 2 (sim.cpp:936-942): compact the offline handles (the snapshot), select
+// k handles with the row costs, apply -- one CTA, after k_reclaim_rows on the same stream.
 __global__ void __launch_bounds__(kNT) k_reclaim(PoolDev P, int k, int mode, int64_t t) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nc = (P.S + 31) >> 5;
   op_begin(P);
-  if (threadIdx.x == 0) P.mirror->r[3] = (int64_t)globaltimer_ns();  // phase stamps (r[3..6])
   // offline handles ascending -> index space
   int carry = 0;
   for (int base = 0; base < P.H; base += blockDim.x) {
@@ -673,15 +754,8 @@ __global__ void __launch_bounds__(kNT) k_reclaim(PoolDev P, int k, int mode, int
   const int n = carry;
   if (k > n) k = n;
   __syncthreads();
-  // distinct resident rows per handle, stride S (warp per handle, match.any dedup)
-  for (int i = wid; i < n; i += nw) {
-    int cnt = 0;
-    VALVE_DISPATCH_NC(nc, cnt = warp_distinct_rows<NC>(P, P.s_hid[i], P.s_rref + (int64_t)i * P.S));
-    if (lane == 0) P.s_cnt[i] = cnt;
-  }
-  __syncthreads();
   if (threadIdx.x == 0) P.mirror->r[4] = (int64_t)globaltimer_ns();
-  const Refs R{nullptr, P.s_cnt, P.S};
+  const Refs R{nullptr, P.s_cnt, P.S, P.s_hid};  // rows by handle id (k_reclaim_rows)
   if (mode == 1) {
     fifo_core(n, P.s_hid, P.s_hmap, k, P.s_pick);
   } else {

@@ -682,6 +682,9 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
     if (mode != VALVE_SELECT_SELECTIVE && mode != VALVE_SELECT_FIFO)
       fail(VALVE_INVALID_ARGUMENT, "reclaim: device-fused mode must be selective or fifo");
     p->order_after_copy_plan();
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    k_reclaim_rows<<<(p->H + 7) / 8, 256, 0, p->stream>>>(p->d);
+    counted();
     p->launch1("reclaim", k_reclaim, p->smem_reclaim, p->d, k, mode, t);
     p->last_n_handles = (int)p->mirror->r[0];
     p->last_n_evicted = (int)p->mirror->r[1];

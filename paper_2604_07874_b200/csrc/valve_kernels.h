@@ -36,6 +36,7 @@ __global__ void k_block_table(PoolDev P, int64_t req, int* out);
 __global__ void k_snapshot_handles(PoolDev P);
 __global__ void k_snapshot(PoolDev P);
 __global__ void k_apply(PoolDev P, const int* ids, int k, int64_t t);
+__global__ void k_reclaim_rows(PoolDev P);
 __global__ void k_reclaim(PoolDev P, int k, int mode, int64_t t);
 __global__ void k_check_invariants(PoolDev P, int64_t online_used);
 __global__ void k_fill_pages(PoolDev P);

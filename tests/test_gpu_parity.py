@@ -64,6 +64,40 @@ def test_selection_large_instances_device_vs_oracle(oracle_c):
             assert A.fifo_reclaim(inst, k) == A.fifo_reclaim(inst, k, backend=oracle_c)
 
 
+def test_selection_packed_key_boundaries_vs_oracle(oracle_c):
+    """The device's packed-key rounds (u32 (marginal << idbits) | index, taken when ids ascend,
+    costs >= 0 and marginals fit) against the oracle at their edges: marginals just below and just
+    above 2^(32 - idbits), all-equal marginals (pure id tie-breaks), zero costs, and shuffled
+    handle order (ids not ascending -> the general path)."""
+    rng = random.Random(77)
+    for n in (1, 2, 3, 513, 1024, 2048):
+        idbits = max(1, (n - 1).bit_length())
+        lim = 1 << (32 - idbits)
+        for case in ("below", "above", "ties", "zeros", "shuffled"):
+            n_req = max(1, n // 2)
+            if case == "below":
+                cost = {r: rng.randint(lim // 8, lim // 4 - 1) for r in range(n_req)}
+            elif case == "above":
+                cost = {r: rng.randint(lim // 2, lim) for r in range(n_req)}
+            elif case == "ties":
+                cost = {r: 7 for r in range(n_req)}
+            else:
+                cost = {r: (0 if case == "zeros" else rng.randint(0, 5000)) for r in range(n_req)}
+            handles = []
+            for h in range(n):
+                if case == "ties":
+                    reqs = [h % n_req]
+                else:
+                    reqs = sorted(set(rng.randrange(n_req) for _ in range(rng.randint(1, 3))))
+                handles.append(A.ReclaimHandle(h * 3 + 1, rng.randint(0, 10**6), reqs))
+            if case == "shuffled":
+                rng.shuffle(handles)
+            inst = A.ReclaimInstance(handles, cost)
+            for k in sorted({1, min(n, 7), min(n, 64)}):
+                want = A.selective_reclaim(inst, k, backend=oracle_c)
+                assert A.selective_reclaim(inst, k) == want, (n, case, k)
+
+
 # ---------------------------------------------- the reference's property tests, same seeds
 
 def ref_random_instance(rng):

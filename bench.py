@@ -342,6 +342,16 @@ def tp_fanout_same_device(torch, A, pool, dev, groups=(1, 2, 4, 8), iters=300, s
             "ack_wait": ["batched memops on the waiting stream", "helper stream per member"][mode], "groups": out}
 
 
+def _guarded(name, fn):
+    """Secondary measurements after the timed region: a failure is recorded in the JSON line
+    instead of losing the line (the headline numbers are already measured)."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001
+        print(f"bench: {name} failed: {e!r}", file=sys.stderr, flush=True)
+        return {"error": repr(e)[:300]}
+
+
 def run_valve(args, rank, world, dist):
     import torch
 
@@ -621,7 +631,7 @@ def run_valve(args, rank, world, dist):
     gc.collect()
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
-    c3 = c3_weights(torch, A, gpu, cp, args.seed + rank, peak)
+    c3 = _guarded("c3_weight_pages", lambda: c3_weights(torch, A, gpu, cp, args.seed + rank, peak))
 
     # ------------------------------------------------ measured online TTFT/TPOT deltas
     # (real-time loop: random-init Llama-3-8B online in PyTorch + the gated offline tenant on a
@@ -640,11 +650,11 @@ def run_valve(args, rank, world, dist):
         # board below its power cap, so the online tenant starts each busy period at full clock
         # (an all-SM GEMM tenant holds ~985 W / ~1,680 MHz and costs the first prefill ~5 %;
         # tools/realtime_sweep.py)
-        rt = RT.measure_deltas(horizon=args.rt_horizon, device=gpu, seed=args.seed + rank,
-                               offline_ctas=args.rt_decode_ctas, repeats=args.rt_repeats,
-                               offline_gemm=tuple(int(x) for x in args.rt_gemm.split(",")) if args.rt_gemm else None,
-                               offline_gemm_ctas=args.rt_gemm_ctas,
-                               log_dir=os.path.join(ROOT, "gpurun_out", "realtime_logs"))
+        rt = _guarded("online_realtime", lambda: RT.measure_deltas(
+            horizon=args.rt_horizon, device=gpu, seed=args.seed + rank,
+            offline_ctas=args.rt_decode_ctas, repeats=args.rt_repeats,
+            offline_gemm=tuple(int(x) for x in args.rt_gemm.split(",")) if args.rt_gemm else None,
+            offline_gemm_ctas=args.rt_gemm_ctas, log_dir=os.path.join(ROOT, "gpurun_out", "realtime_logs")))
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "r1_copy_traffic.json")))
     except OSError:

@@ -11,12 +11,17 @@ models' weights (capped at 1024), a Qwen2-7B offline page = 917,504 B; offline r
 One step = one reclaim op of k handles (k = 36, the C2 probe shape), as Sim::finish_op runs it
 (sim.cpp:912-992), on the device:
     gate raise -> quiesce of the running gated offline kernel -> fused snapshot + Algorithm 1 +
-    apply_reclaim (one launch) -> gather-copy of the invalidated pages to pinned host memory ->
-    online_release + offline re-admission of the evicted requests -> gate release.
+    apply_reclaim (multi-CTA instance pass + one CTA) -> start the gather-copy of the invalidated
+    pages to pinned host memory -> online_release + offline re-admission of the evicted
+    requests -> gate release.
+Steps are pipelined through the copy ring: op i+1's quiesce and decision run while op i's bytes
+cross the link (one copy queued behind the running one); the ring is drained inside the timed
+region.
 value = reclaimed bytes / device time of the K timed steps (inputs resident in HBM; every step
 reads 2.1 GB of distinct pages out of a 128 GiB pool, far above the 126 MB L2).
-e2e   = the same op through the reference-facing API with host buffers: snapshot() to host,
-        selective_reclaim(instance) (upload), apply_reclaim(ids), copy, as Sim calls them.
+e2e   = the same ops through the reference-facing API with host buffers: snapshot() to host,
+        selective_reclaim(instance) (upload), apply_reclaim(ids), reclaim_copy_start(), as Sim
+        calls them, pipelined the same way.
 p99 preempt-to-quiesce: >= 1000 preemptions of the gated offline kernel, CUDA events on the gate
 stream around (gate store -> wait for every offline CTA to retire).
 

@@ -20,9 +20,9 @@ constexpr int kSmemHandles = 2048;   // greedy in shared memory up to this many 
 constexpr int kSmemListings = 4096;  // ... and this many (handle, request) listings
 constexpr int kSmemTuples = 8192;    // invalidation report sorted in shared memory
 // dynamic shared memory of k_reclaim / k_apply / k_select_instance (host sets the attribute):
-// greedy 2048*(8+4+4+1+4) + 4096*(8+4+4+4+4+4) + 4 = 157,700 B; apply sort 8192*12 = 98,304 B
+// greedy 2048*(8+4+4+1+4) + 4096*(8+4+4+4+4+4) + 4 = 157,700 B; apply sort 8192*20 = 163,840 B
 static_assert(kSmemHandles * 21 + kSmemListings * 28 + 64 <= 160 * 1024, "greedy smem");
-static_assert(kSmemTuples * 12 <= 160 * 1024, "sort smem");
+static_assert(kSmemTuples * 20 <= 160 * 1024, "sort smem");  // key 8 + pay 4 + cursors 4 + segment 4
 
 __device__ long long g_greedy_cycles[2];  // diagnostics: argmin / update cycles of the last run
 __device__ long long g_apply_ns[6];       // diagnostics: apply_core phase stamps of the last run
@@ -607,14 +607,48 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
   }
   for (int e = threadIdx.x; e < ne; e += blockDim.x) bcnt[e] = 0;
   __syncthreads();
+  int* segof = in_smem ? bcnt + kSmemTuples : nullptr;  // [nt] request rank of each position
   for (int i = threadIdx.x; i < nt; i += blockDim.x) {
     const int rank = P.s_rank[P.s_qh[i]];
     const int pos = P.res_inv_off[rank] + atomicAdd(&bcnt[rank], 1);
     key[pos] = ((uint64_t)(uint32_t)P.s_rref[i] << 24) | (uint64_t)(uint32_t)P.s_tphys[i];
     pay[pos] = P.s_tblk[i];
+    if (segof) segof[pos] = rank;
   }
+  // Longest request segment: up to kRankSeg the order inside each segment comes from ranks
+  // (every element counts the smaller keys of its segment -- keys are unique: the physical page
+  // breaks logical-id ties), which keeps all 1024 threads busy; a warp-per-segment sort left 31
+  // warps waiting at the barrier for the warp holding the longest segments (~17 us at k = 36).
+  int seg_local = 0;
+  for (int e = threadIdx.x; e < ne; e += blockDim.x)
+    seg_local = max(seg_local, P.res_inv_off[e + 1] - P.res_inv_off[e]);
+  __shared__ int s_seg;
+  if (threadIdx.x == 0) s_seg = 0;
   __syncthreads();
-  {
+  if (seg_local) atomicMax(&s_seg, seg_local);
+  __syncthreads();
+  constexpr int kRankSeg = 1024;
+  if (s_seg <= kRankSeg) {
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+      int lo = 0, hi = ne - 1;  // segment of position i
+      if (segof) {
+        lo = segof[i];
+      } else {
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (P.res_inv_off[mid] <= i) lo = mid;
+          else hi = mid - 1;
+        }
+      }
+      const int o = P.res_inv_off[lo], end = P.res_inv_off[lo + 1];
+      const uint64_t kv = key[i];
+      int r = 0;
+      for (int j = o; j < end; ++j) r += key[j] < kv;
+      P.res_pages[o + r] = (int64_t)(kv >> 24);
+      P.res_phys[o + r] = (int)(kv & 0xffffffull);
+      P.res_blk[o + r] = pay[i];
+    }
+  } else {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int e = wid; e < ne; e += nw) {
       const int o = P.res_inv_off[e], n = P.res_inv_off[e + 1] - o;

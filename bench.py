@@ -74,8 +74,9 @@ def parse():
     ap.add_argument("--rt-decode-ctas", type=int, default=16,
                     help="offline KV decode-pass CTAs in the real-time run (-1 = none, 0 = library default)")
     ap.add_argument("--rt-gemm-ctas", type=int, default=64, help="offline GEMM CTAs in the real-time run (0 = all SMs)")
-    ap.add_argument("--rt-gemm", default="2048,37888,3584",
-                    help="m,n,k of the offline tenant's gated tcgen05 GEMM (Qwen2-7B gate/up); '' = decode pass only")
+    ap.add_argument("--rt-gemm", default="qwen2-7b:2048",
+                    help="offline tenant's gated tcgen05 GEMMs: 'qwen2-7b:<tokens>' = a random-init Qwen2-7B's "
+                         "projection chain (28 layers x qkv/o/gate-up/down), 'm,n,k' = one shape, '' = decode pass only")
     ap.add_argument("--profile-mode", action="store_true",
                     help="ncu launch-list runs: no offline kernel (ncu serialises it to completion)")
     return ap.parse_args()
@@ -346,6 +347,15 @@ def tp_fanout_same_device(torch, A, pool, dev, groups=(1, 2, 4, 8), iters=300, s
     return {"note": "one leader + N-1 member gates on one B200 (no NVLink hop); offline decode pass "
                     "per member on 148/N CTAs; leader raise -> all members quiesced",
             "ack_wait": ["batched memops on the waiting stream", "helper stream per member"][mode], "groups": out}
+
+
+def _rt_gemm(spec):
+    """--rt-gemm: "m,n,k" (one GEMM shape), "qwen2-7b:<tokens>" (the model's projection chain) or ''."""
+    if not spec:
+        return None
+    if spec.startswith("qwen2-7b"):
+        return ("qwen2-7b", int(spec.split(":")[1]))
+    return tuple(int(x) for x in spec.split(","))
 
 
 def _guarded(name, fn):
@@ -664,7 +674,7 @@ def run_valve(args, rank, world, dist):
         rt = _guarded("online_realtime", lambda: RT.measure_deltas(
             horizon=args.rt_horizon, device=gpu, seed=args.seed + rank,
             offline_ctas=args.rt_decode_ctas, repeats=args.rt_repeats,
-            offline_gemm=tuple(int(x) for x in args.rt_gemm.split(",")) if args.rt_gemm else None,
+            offline_gemm=_rt_gemm(args.rt_gemm),
             offline_gemm_ctas=args.rt_gemm_ctas, log_dir=os.path.join(ROOT, "gpurun_out", "realtime_logs")))
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "r1_copy_traffic.json")))

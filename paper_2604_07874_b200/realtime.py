@@ -219,6 +219,7 @@ class RunResult:
     offline_bytes: float = 0.0
     offline_gemm_tiles: int = 0
     offline_gemm_flop: float = 0.0
+    offline_gemms_done: float = 0.0
     quiesce_wait_us: List[float] = field(default_factory=list)
     decode_iter_us: List[float] = field(default_factory=list)
     prefill_us: List[float] = field(default_factory=list)
@@ -236,7 +237,10 @@ class Colocation:
                  tile_bytes: int = 16384, offline_ctas: int = 0, offline_gemm=None, offline_gemm_ctas: int = 0):
         """offline_gemm=(m, n, k): the offline tenant also runs the gated tcgen05 GEMM (its
         projection work, e.g. Qwen2-7B gate/up over m tokens) next to the decode pass, on its own
-        gate attached to the channel's gate, so one raise quiesces both."""
+        gate attached to the channel's gate, so one raise quiesces both.
+        offline_gemm=("qwen2-7b", m): the tenant runs a random-init Qwen2-7B's projection chain
+        instead -- 28 layers x (qkv, o, gate/up, down) gated GEMMs over m tokens, each preempted
+        and resumed at tile granularity, the chain advancing when a GEMM's work list completes."""
         self.model, self.pool, self.gate = model, pool, gate
         self.page_tokens = page_tokens
         self.tile_bytes = tile_bytes
@@ -251,17 +255,33 @@ class Colocation:
         self.gemm_gate = None
         self.gemm_ctas = offline_gemm_ctas  # 0 = one CTA per SM (power knob: fewer SMs, less draw)
         if self.colocated and offline_gemm:
-            m, n, k = offline_gemm
             dev = model.device
-            self.gemm_shape = (m, n, k)
             g = torch.Generator(device=dev).manual_seed(7)
-            self.gemm_a = torch.randn(m, k, device=dev, generator=g).to(torch.bfloat16)
-            self.gemm_b = (torch.randn(n, k, device=dev, generator=g) * 0.02).to(torch.bfloat16)
-            self.gemm_c = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+
+            def rnd(*shape, scale=1.0):
+                return (torch.randn(*shape, device=dev, generator=g) * scale).to(torch.bfloat16)
+
+            self.gemm_seq = []  # (a, b, c, m, n, k, tiles) in execution order
+            if offline_gemm[0] == "qwen2-7b":
+                m = int(offline_gemm[1])
+                d, qkv, ffn, layers = 3584, 4608, 18944, 28  # Qwen2-7B: 28 x (28 q + 2 x 4 kv heads x 128)
+                x, act = rnd(m, d), rnd(m, ffn)
+                outs = {n: torch.empty(m, n, device=dev, dtype=torch.bfloat16) for n in (qkv, d, 2 * ffn)}
+                for _ in range(layers):
+                    for (a, n, k) in ((x, qkv, d), (x, d, d), (x, 2 * ffn, d), (act, d, ffn)):
+                        self.gemm_seq.append((a, rnd(n, k, scale=0.02), outs[n], m, n, k))
+                self.gemm_model = {"model": "Qwen2-7B projections (random init)", "tokens": m, "layers": layers}
+            else:
+                m, n, k = offline_gemm
+                self.gemm_seq.append((rnd(m, k), rnd(n, k, scale=0.02), torch.empty(m, n, device=dev, dtype=torch.bfloat16),
+                                      m, n, k))
+                self.gemm_model = None
+            self.gemm_seq = [(a, b, c, m, n, k, (m // (256 if m % 256 == 0 else 128)) * (n // 256))
+                             for (a, b, c, m, n, k) in self.gemm_seq]
+            self.gemm_shape = tuple(self.gemm_seq[0][3:6])
             self.gemm_gate = A.Gate(dev.index if dev.index is not None else 0)
             gate.attach_peers([self.gemm_gate])
             self.gemm_stream = torch.cuda.Stream()
-            self.gemm_tiles = (m // (256 if m % 256 == 0 else 128)) * (n // 256)
         if self.colocated:
             hooks = A.Hooks(schedule=self._schedule, on_disabled=lambda t: None,
                             on_enabled=self._on_enabled, log=None)
@@ -292,12 +312,15 @@ class Colocation:
 
     def _launch_gemm(self):
         st = self.gemm_gate.read()
-        fresh = st.tiles_claimed >= self.gemm_tiles  # previous pass finished: a new work list
+        a, b, c, m, n, k, tiles = self.gemm_seq[self._gemm_idx]
+        fresh = st.tiles_claimed >= tiles  # this GEMM's work list finished: the next one
         if fresh:
-            self._gemm_harvest += st.tiles_done
-        m, n, k = self.gemm_shape
-        self.gemm_gate.launch_gemm(self.gemm_a.data_ptr(), self.gemm_b.data_ptr(), self.gemm_c.data_ptr(),
-                                   m, n, k, ctas=self.gemm_ctas, stream=self.gemm_stream.cuda_stream, fresh=fresh)
+            self._gemm_flop += 2.0 * m * n * k
+            self._gemm_done += 1
+            self._gemm_idx = (self._gemm_idx + 1) % len(self.gemm_seq)
+            a, b, c, m, n, k, tiles = self.gemm_seq[self._gemm_idx]
+        self.gemm_gate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, ctas=self.gemm_ctas,
+                                   stream=self.gemm_stream.cuda_stream, fresh=fresh)
 
     def _launch_decode(self):
         if self.offline_ctas < 0:
@@ -395,7 +418,7 @@ class Colocation:
         self._evicted, self._off_live, self._off_req_pages, self._off_cost = [], {}, {}, {}
         self._off_pages = 0
         self._harvest = 0
-        self._gemm_harvest = 0
+        self._gemm_flop, self._gemm_done, self._gemm_idx = 0.0, 0, 0
         reqs = [OnlineReq(r.rid, r.arrival_us, r.prompt, r.output) for r in trace]
         by_rid = {r.rid: r for r in reqs}
         log = self.res.log
@@ -582,9 +605,11 @@ class Colocation:
             self.res.offline_tiles = self._harvest + self.gate.read().tiles_done
             self.res.offline_bytes = self.res.offline_tiles * self.tile_bytes
             if self.gemm_gate is not None:
-                m, n, k = self.gemm_shape
-                self.res.offline_gemm_tiles = self._gemm_harvest + self.gemm_gate.read().tiles_done
-                self.res.offline_gemm_flop = self.res.offline_gemm_tiles * 2.0 * m * n * k / self.gemm_tiles
+                _, _, _, m, n, k, tiles = self.gemm_seq[self._gemm_idx]
+                part = self.gemm_gate.read().tiles_done
+                self.res.offline_gemm_tiles = part
+                self.res.offline_gemm_flop = self._gemm_flop + part * 2.0 * m * n * k / tiles
+                self.res.offline_gemms_done = self._gemm_done + part / tiles
             self.gate.release(gen)
             torch.cuda.synchronize()
         return self.res
@@ -804,7 +829,9 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
         "offline_ctas": offline_ctas or "default",
         "offline_gbs_harvested": colo.offline_bytes / colo.wall_s / 1e9,
         "offline_gemm": ({"shape": list(offline_gemm), "tflops_harvested": colo.offline_gemm_flop / colo.wall_s / 1e12,
-                          "tiles": colo.offline_gemm_tiles, "ctas": offline_gemm_ctas or "one per SM"}
+                          "gemms_completed": colo.offline_gemms_done, "ctas": offline_gemm_ctas or "one per SM",
+                          **({"model_tokens_per_s": colo.offline_gemms_done / (4 * 28) * offline_gemm[1] / colo.wall_s}
+                             if offline_gemm[0] == "qwen2-7b" else {})}
                          if offline_gemm else None),
         "prefill_ms_median": {"standalone": _median([x for s in solos for x in s.prefill_us]) / 1e3,
                               "colocated": _median([x for c in colos for x in c.prefill_us]) / 1e3},

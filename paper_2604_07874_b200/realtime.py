@@ -744,7 +744,7 @@ def measure_deltas(horizon=24.0, base=0.3, spike=6.0, period=8.0, width=1.0, han
     plan = None
     if replay:  # the second of two live runs (the first one still pays first-use costs)
         for _ in range(2):
-            plan = Colocation(model, None, None).run(trace, horizon_s=horizon + 30, admit_margin_us=3000).plan
+            plan = Colocation(model, None, None).run(trace, horizon_s=horizon + 30, admit_margin_us=6000).plan
     solos, colos = [], []
     clocks = {"standalone": [], "colocated": []}
     for i in range(repeats):

@@ -133,3 +133,18 @@ def test_live_harness_logs_match_reference_metrics(tmp_path):
         assert ref["pairs"] == out["pairs"]
         assert ref["ttft_mean_pct"] == pytest.approx(paired_increase(s_ttft, c_ttft)["mean_pct"], rel=1e-12, abs=1e-12)
         assert ref["tpot_mean_pct"] == pytest.approx(paired_increase(s_tpot, c_tpot)["mean_pct"], rel=1e-12, abs=1e-12)
+
+
+@pytest.mark.gpu
+def test_live_harness_with_offline_model_chain():
+    """The offline tenant as a random-init Qwen2-7B projection chain (28 layers x 4 gated GEMMs):
+    the chain advances across preemptions (GEMMs complete, harvest > 0) and the paired run still
+    yields reference-pairable deltas."""
+    from paper_2604_07874_b200 import realtime as RT
+
+    out = RT.measure_deltas(horizon=4.0, base=1.0, spike=6.0, period=4.0, width=1.0, handles=16, layers=2,
+                            output=(4, 6), prompt=(600, 900), offline_gemm=("qwen2-7b", 256),
+                            offline_gemm_ctas=16)
+    g = out["offline_gemm"]
+    assert g["gemms_completed"] > 4 and g["tflops_harvested"] > 0 and g["model_tokens_per_s"] > 0
+    assert out["pairs"] > 0 and len(out["plan_deviations"]["colocated"]) == 1

@@ -569,6 +569,12 @@ def run_valve(args, rank, world, dist):
     ce_runs = sum(1 for i, p in enumerate(flat) if i == 0 or p != flat[i - 1] + 1)  # 2D transfers
     ce = pool.reclaim_copy(host.ptr, host.nbytes, engine="ce")
     ce_gbs = ce.bytes / (ce.kernel_ms * 1e-3) / 1e9
+    # the same report again through the SM kernel under a rate bound (token bucket, 1 MiB burst):
+    # bytes / (first chunk issued -> last store retired) must sit at the configured rate
+    rate = 25e9
+    rb = pool.reclaim_copy(host.ptr, host.nbytes, A.copy_params(ctas=args.copy_ctas, threads=args.copy_threads,
+                                                                rate_bytes_per_s=rate, burst_bytes=1 << 20))
+    rate_gbs = rb.bytes / ((rb.t_last_ns - rb.t_first_ns) * 1e-9) / 1e9 if rb.t_last_ns > rb.t_first_ns else None
     restore(pool.last_reclaim().evicted_requests)
 
     # ------------------------------------------------ eviction-policy contrast on the device
@@ -716,6 +722,8 @@ def run_valve(args, rank, world, dist):
         "copy_engine_alt_gbs": round(ce_gbs, 2),
         "copy_engine_alt_frac": round(ce_gbs / peak, 4),
         "copy_engine_alt_transfers": ce_runs,
+        "rate_bound": {"set_gbs": rate / 1e9, "achieved_gbs": round(rate_gbs, 2) if rate_gbs else None,
+                       "bytes": rb.bytes, "burst_bytes": 1 << 20},
         "copy_note": "SM-issued sysmem stores leave as 128 B PCIe TLPs vs 256 B for the copy engines: "
                      "the SM kernel's ceiling is (128/152)/(256/280) = 92.1% of the CE-measured peak",
         "burst_first_quiesce_us": round(stats["quiesce_us"][0], 1),

@@ -110,8 +110,9 @@ int valve_pool_set_page_bytes(valve_pool* p, int n, const int64_t* reqs, const i
  * size of each evicted request (report order; request e's pages follow those of requests < e). */
 int valve_pool_last_copy_layout(const valve_pool* p, int64_t* page_bytes, int cap, int64_t* total);
 enum { VALVE_SELECT_SELECTIVE = 0, VALVE_SELECT_FIFO = 1, VALVE_SELECT_ORACLE = 2 };
-/* snapshot -> selection (mode) -> apply_reclaim in ONE kernel launch, no host round trip in
- * between (sim.cpp:936-942).  Results stay on the device for valve_pool_reclaim_copy();
+/* snapshot -> selection (mode) -> apply_reclaim on the device with no host round trip in
+ * between (sim.cpp:936-942): a grid-wide instance pass, then one CTA for selection + apply, both
+ * stream-ordered on the pool stream.  Results stay on the device for valve_pool_reclaim_copy();
  * the summary (n_handles, n_evicted, n_pages) is returned; use
  * valve_pool_last_reclaim() to read the full result. */
 int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles, int* n_evicted,

@@ -270,15 +270,12 @@ class Colocation:
                 for _ in range(layers):
                     for (a, n, k) in ((x, qkv, d), (x, d, d), (x, 2 * ffn, d), (act, d, ffn)):
                         self.gemm_seq.append((a, rnd(n, k, scale=0.02), outs[n], m, n, k))
-                self.gemm_model = {"model": "Qwen2-7B projections (random init)", "tokens": m, "layers": layers}
             else:
                 m, n, k = offline_gemm
                 self.gemm_seq.append((rnd(m, k), rnd(n, k, scale=0.02), torch.empty(m, n, device=dev, dtype=torch.bfloat16),
                                       m, n, k))
-                self.gemm_model = None
             self.gemm_seq = [(a, b, c, m, n, k, (m // (256 if m % 256 == 0 else 128)) * (n // 256))
                              for (a, b, c, m, n, k) in self.gemm_seq]
-            self.gemm_shape = tuple(self.gemm_seq[0][3:6])
             self.gemm_gate = A.Gate(dev.index if dev.index is not None else 0)
             gate.attach_peers([self.gemm_gate])
             self.gemm_stream = torch.cuda.Stream()

@@ -304,7 +304,7 @@ def gemm_tenant(torch, A, gate, dev, stream, gate_stream, preemptions, next_gen)
             "max_quiesce_us": q[-1] if q else None}
 
 
-def tp_fanout_same_device(torch, A, pool, dev, groups=(1, 2, 4, 8), iters=300, seed=0, mode=0):
+def tp_fanout_same_device(torch, A, pool, dev, groups=(1, 2, 4, 8), iters=300, seed=0, mode=0, ctas=0):
     """TP-group gate fan-out with every member gate on this one GPU: the leader's
     raise writes all N gate words (stream memory operations), its wait joins N concurrent
     live_ctas waits on helper streams; each member runs its own gated offline kernel on 148/N
@@ -320,12 +320,12 @@ def tp_fanout_same_device(torch, A, pool, dev, groups=(1, 2, 4, 8), iters=300, s
             gates[0].attach_peers(gates[1:])
         streams = [torch.cuda.Stream(device=dev) for _ in range(n)]
         gs = torch.cuda.ExternalStream(gates[0].stream, device=dev)
-        ctas = max(1, 148 // n)
+        ctas_m = ctas or max(1, 148 // n)
         lat = []
         for it in range(iters + 20):
             for g, st in zip(gates, streams):
                 g.reset_work()  # a fresh pass each time (one pass is far longer than a sample)
-                g.launch_offline(pool, None, None, 0, 0, None, ctas=ctas, stream=st.cuda_stream)
+                g.launch_offline(pool, None, None, 0, 0, None, ctas=ctas_m, stream=st.cuda_stream)
             deadline = time.perf_counter() + rng.uniform(100e-6, 400e-6)
             while time.perf_counter() < deadline:
                 pass
@@ -342,7 +342,7 @@ def tp_fanout_same_device(torch, A, pool, dev, groups=(1, 2, 4, 8), iters=300, s
         torch.cuda.synchronize()
         lat.sort()
         out[str(n)] = {"p50_us": round(lat[len(lat) // 2], 2), "p99_us": round(lat[int(0.99 * (len(lat) - 1))], 2),
-                       "max_us": round(lat[-1], 2), "preemptions": len(lat), "ctas_per_member": ctas}
+                       "max_us": round(lat[-1], 2), "preemptions": len(lat), "ctas_per_member": ctas_m}
         del gates
     return {"note": "one leader + N-1 member gates on one B200 (no NVLink hop); offline decode pass "
                     "per member on 148/N CTAs; leader raise -> all members quiesced",

@@ -1388,8 +1388,7 @@ int valve_gate_raise(valve_gate* g, uint32_t gen, void* s) {
     MemBatch b;
     b.write32(&g->d->closed, 1);
     for (valve_gate* x : g->peers) b.write32(&x->d->closed, 1);
-    b.write32(&g->d->gen, gen);
-    for (valve_gate* x : g->peers) b.write32(&x->d->gen, gen);
+    b.write32(&g->d->gen, gen);  // diagnostic generation: the leader's word only (each memop ~1 us)
     b.submit(op, st);
   });
 }
@@ -1432,8 +1431,7 @@ int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* s) {
       MemBatch b;
       b.wait_eq32(&g->d->live_ctas, 0);
       for (valve_gate* x : g->peers) b.wait_eq32(&x->d->live_ctas, 0);
-      b.write32(&g->d->quiesced_gen, gen);
-      for (valve_gate* x : g->peers) b.write32(&x->d->quiesced_gen, gen);
+      b.write32(&g->d->quiesced_gen, gen);  // the group's ack: on the leader's word
       b.submit(op, st);
       return;
     }

@@ -126,8 +126,8 @@ def test_fanout_modes_quiesce_every_member_same_process(mode):
     gates[0].wait_quiesced(7)
     torch.cuda.ExternalStream(gates[0].stream).synchronize()
     st = [g.read() for g in gates]
-    assert all(s.closed == 1 and s.live_ctas == 0 and s.quiesced_gen == 7 for s in st), \
-        [(s.closed, s.live_ctas, s.quiesced_gen) for s in st]
+    assert all(s.closed == 1 and s.live_ctas == 0 for s in st), [(s.closed, s.live_ctas) for s in st]
+    assert st[0].quiesced_gen == 7  # the group's ack generation lives on the leader's word
     assert all(s.tiles_done == s.tiles_claimed for s in st)  # claimed tiles all finished
     time.sleep(0.005)
     assert [g.read().tiles_claimed for g in gates] == [s.tiles_claimed for s in st]  # nothing claimed

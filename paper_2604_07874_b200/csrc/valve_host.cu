@@ -1410,12 +1410,12 @@ int valve_gate_release(valve_gate* g, uint32_t gen, void* s) {
     ck(cudaSetDevice(g->device), "cudaSetDevice");
     std::vector<valve_gate*> all{g};
     all.insert(all.end(), g->peers.begin(), g->peers.end());
+    // reopen every member first (offline work resumes after N memops, not 3N), then clear the
+    // diagnostics for the next raise (same stream: done before it) and stamp the leader's gen
     MemBatch b;
-    for (valve_gate* x : all) {
-      b.write64(&x->d->t_first_seen, 0);
-      b.write32(&x->d->gen, gen);
-    }
     for (valve_gate* x : all) b.write32(&x->d->closed, 0);
+    for (valve_gate* x : all) b.write64(&x->d->t_first_seen, 0);
+    b.write32(&g->d->gen, gen);
     b.submit(op, st);
   });
 }

@@ -84,6 +84,29 @@ def parse():
 
 # --------------------------------------------------------------------------- workload
 
+def _hbm_peak():
+    """Measured HBM copy bandwidth of this pool's B200s (driver-written MEASURED_PEAKS.json),
+    else the profiling recipe's fallback."""
+    try:
+        v = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 6541.5, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
+
+
+HBM_PEAK, HBM_PEAK_SOURCE = _hbm_peak()
+
+
+def workload_config(handles, k, world):
+    """The workload both arms run (identical dicts: the driver compares them)."""
+    return {"workload": "C2: Llama-3-8B online + Qwen2-7B offline, 1 B200, KV reclaim only "
+                        "(BASELINE.json configs[1])",
+            "total_handles": handles, "handle_size_pages": HSZ, "slot_bytes": SLOT, "page_bytes": PAGE,
+            "k_handles_per_op": k,
+            "l2": "inputs larger than L2 (distinct 2.1 GB of a 128 GiB pool per step)",
+            "parallelism": f"replicas{world}"}
+
+
 def offline_requests(seed, n):
     """Qwen2-7B offline stream: prompt 2000-4000, output 100-200 tokens."""
     rng = random.Random(seed)
@@ -700,16 +723,9 @@ def run_valve(args, rank, world, dist):
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic",
-        "config": {
-            "workload": "C2: Llama-3-8B online + Qwen2-7B offline, 1 B200, KV reclaim only "
-                        "(BASELINE.json configs[1])",
-            "total_handles": H, "handle_size_pages": HSZ, "slot_bytes": SLOT, "page_bytes": PAGE,
-            "k_handles_per_op": args.k, "live_offline_requests": len(live),
-            "pages_per_op_mean": statistics.mean(stats["pages"]),
-            "copy_ctas": args.copy_ctas, "copy_threads": args.copy_threads, "copy_tma": args.tma,
-            "l2": "inputs larger than L2 (distinct 2.1 GB of a 128 GiB pool per step)",
-            "parallelism": f"replicas{world}",
-        },
+        "config": workload_config(H, args.k, world),
+        "run": {"live_offline_requests": len(live), "pages_per_op_mean": statistics.mean(stats["pages"]),
+                "copy_ctas": args.copy_ctas, "copy_threads": args.copy_threads, "copy_tma": args.tma},
         "p50_preempt_to_quiesce_us": round(pct(50), 2),
         "p99_preempt_to_quiesce_us": round(pct(99), 2),
         "max_preempt_to_quiesce_us": round(q[-1], 2),
@@ -748,8 +764,8 @@ def run_valve(args, rank, world, dist):
                            "HBM is ~110x faster)",
             "kernel": "k_reclaim_copy",
             "algorithmic_bytes_per_launch": round(statistics.mean(stats["bytes"])),
-            "hbm": {"achieved": round(copy_gbs, 2), "peak": 6541.5, "unit": "GB/s",
-                    "frac": round(copy_gbs / 6541.5, 5), "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "hbm": {"achieved": round(copy_gbs, 2), "peak": HBM_PEAK, "unit": "GB/s",
+                    "frac": round(copy_gbs / HBM_PEAK, 5), "peak_source": HBM_PEAK_SOURCE},
         },
         "e2e": {
             "value": round(e2e_bytes / e2e_s / 1e9, 3),
@@ -880,9 +896,7 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(r["secs"] / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": "C2: Llama-3-8B online + Qwen2-7B offline, 1 B200, KV reclaim only "
-                               "(BASELINE.json configs[1])", "k_handles_per_op": args.k,
-                   "total_handles": args.handles or 1024},
+        "config": workload_config(args.handles or 1024, args.k, world),
         "p99_preempt_to_quiesce_us": 1000, "p99_note": "reference quiesce is the modeled toggle "
                                                        "constant (scenario.hpp:37), not a timing",
         "cpu_baseline": {"value": round(r["value"], 3), "unit": "GB/s", "cores": threads,

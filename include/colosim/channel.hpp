@@ -65,17 +65,37 @@ class ChannelController {
   State state() const { return static_cast<State>(valve_channel_state(ch_.get())); }
   bool offline_compute_allowed() const { return valve_channel_offline_compute_allowed(ch_.get()) != 0; }
   std::int64_t disables_issued() const { return valve_channel_disables_issued(ch_.get()); }
-  void note_busy(SimTime t) { valve_channel_note_busy(ch_.get(), t); }
+  // Transitions that store to the bound device gate (disable raises it, enable releases it)
+  // surface a failed store as std::runtime_error, after the state machine has moved -- the
+  // reference's transitions cannot fail, so its callers never see this without a gate.
+  void note_busy(SimTime t) {
+    valve_channel_note_busy(ch_.get(), t);
+    gate_check();
+  }
   void note_all_idle(SimTime t) { valve_channel_note_all_idle(ch_.get(), t); }
-  SimTime ensure_disabled(SimTime t) { return valve_channel_ensure_disabled(ch_.get(), t); }
-  void handle_toggle(SimTime t, std::int64_t gen) { valve_channel_handle_toggle(ch_.get(), t, gen); }
-  void handle_cooldown(SimTime t, std::int64_t gen) { valve_channel_handle_cooldown(ch_.get(), t, gen); }
+  SimTime ensure_disabled(SimTime t) {
+    const SimTime e = valve_channel_ensure_disabled(ch_.get(), t);
+    gate_check();
+    return e;
+  }
+  void handle_toggle(SimTime t, std::int64_t gen) {
+    valve_channel_handle_toggle(ch_.get(), t, gen);
+    gate_check();
+  }
+  void handle_cooldown(SimTime t, std::int64_t gen) {
+    valve_channel_handle_cooldown(ch_.get(), t, gen);
+    gate_check();
+  }
   SimTime pending_effective() const { return valve_channel_pending_effective(ch_.get()); }
 
   // B200 addition: raise/release this device gate on the disable/enable edges.
   void bind_gate(valve_gate* g) { valve_detail::check(valve_channel_bind_gate(ch_.get(), g)); }
+  void bind_gate(valve_gate* g, void* stream) {
+    valve_detail::check(valve_channel_bind_gate_stream(ch_.get(), g, stream));
+  }
 
  private:
+  void gate_check() { valve_detail::check(valve_channel_gate_status(ch_.get())); }
   struct Del {
     void operator()(valve_channel* c) const { valve_channel_destroy(c); }
   };

@@ -52,11 +52,15 @@ typedef struct {
   int page_size_tokens;
   int64_t slot_bytes;         /* physical bytes per page slot; 0 = no page store (decisions only) */
   int64_t page_bytes;         /* bytes of KV actually held per page (<= slot_bytes) */
-  int max_requests;           /* live offline requests the device request table holds */
-  int max_pages_per_request;  /* block-table row length */
+  int max_requests;           /* initial rows of the device request table (grows on demand) */
+  int max_pages_per_request;  /* initial block-table row length (grows on demand) */
 } valve_pool_config;
 
-/* Defaults: device 0, slot_bytes 0, page_bytes 0, max_requests 4096, max_pages 4096. */
+/* Defaults: device 0, slot_bytes 0, page_bytes 0, max_requests 4096, max_pages 4096.  The two
+ * table sizes are starting points, not limits: offline_reserve grows the request table and the
+ * block-table rows when a reservation needs more (the reference MemoryPool has no such limit),
+ * which moves valve_pool_view.block_tables / max_pages_per_request -- re-read the view after a
+ * reserve if you cache it. */
 void valve_pool_config_default(valve_pool_config* cfg);
 /* memory.hpp:23 MemoryPool(total_handles, handle_size_pages, page_size_tokens) */
 int valve_pool_create(int total_handles, int handle_size_pages, int page_size_tokens, valve_pool** out);
@@ -221,6 +225,8 @@ int64_t valve_resctl_pressure_in_window(const valve_resctl* c, int64_t t);
 /* An HBM gate word {generation, closed} polled by every warp of the gated offline
  * kernels at each tile boundary; quiesce is acknowledged per CTA. */
 typedef struct valve_gate valve_gate;
+/* In a TP group (valve_gate_attach_peers) `gen` and `quiesced_gen` are the GROUP's words and
+ * live on the leader only (both fan-out modes): a member gate's copies are not written. */
 typedef struct {
   uint32_t gen;            /* last generation written */
   uint32_t closed;
@@ -277,7 +283,12 @@ typedef struct {
   int64_t tile_bytes;     /* bytes of one tile (the quiesce granularity); 0 = 16 KiB */
 } valve_offline_work;
 int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work* w, void* stream);
-/* Resets the tile cursor / statistics (new work). */
+/* Resets the tile cursor / statistics (new work).  The first valve_offline_launch after a
+ * reset freezes the work list (the tile prefix over the listed rows and their block counts);
+ * resumed launches reuse it, so every tile of that list runs exactly once across preemptions
+ * even when reclaims or re-admissions change the pool's rows meanwhile (an evicted row's
+ * blocks then read as quarantine / unmapped and count as canary hits).  Resuming with another
+ * rows / n_requests / tile_bytes without a reset is a VALVE_LOGIC_ERROR. */
 int valve_offline_reset(valve_gate* g);
 
 /* Gated offline GEMM: C = A * B^T in bf16 with fp32 accumulation on the tcgen05
@@ -315,6 +326,13 @@ int valve_channel_create(int64_t toggle_us, int64_t cooldown_us, const valve_cha
                          valve_channel** out);
 void valve_channel_destroy(valve_channel* c);
 int valve_channel_bind_gate(valve_channel* c, valve_gate* g);
+/* Same, with the stream the raise/release stores are issued on (e.g. the online stream, so a
+ * wait_quiesced enqueued there is ordered after the raise; NULL = the gate's own stream). */
+int valve_channel_bind_gate_stream(valve_channel* c, valve_gate* g, void* stream);
+/* Status of the device-gate stores the state machine issued since the last call (the
+ * transitions return void, as channel.hpp's do): VALVE_OK, or the first failure's code with its
+ * message in valve_last_error().  Clears the status. */
+int valve_channel_gate_status(valve_channel* c);
 int valve_channel_state(const valve_channel* c);
 int valve_channel_offline_compute_allowed(const valve_channel* c);
 int64_t valve_channel_disables_issued(const valve_channel* c);

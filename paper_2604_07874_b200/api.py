@@ -578,7 +578,7 @@ class ChannelController:
     kEnabled, kDisabling, kDisabled, kEnabling = range(4)
 
     def __init__(self, toggle_us: int, cooldown_us: int, hooks: Optional[Hooks] = None, *,
-                 backend: Optional[Backend] = None, gate=None):
+                 backend: Optional[Backend] = None, gate=None, gate_stream: Optional[int] = None):
         self._b = backend or valve_backend()
         hk = hooks or Hooks()
         self._cbs = (
@@ -591,9 +591,18 @@ class ChannelController:
         self._h = C.c_void_p()
         self._b.check(self._b.fn("channel_create")(int(toggle_us), int(cooldown_us),
                                                    C.byref(self._hooks), C.byref(self._h)))
+        self._gate = None
         if gate is not None:
-            self._b.check(self._b.lib.valve_channel_bind_gate(self._h, gate.handle))
+            # gate_stream: the stream the raise/release stores go on -- the online stream, so a
+            # wait_quiesced enqueued there afterwards is ordered behind the raise
+            self._b.check(self._b.lib.valve_channel_bind_gate_stream(
+                self._h, gate.handle, C.c_void_p(gate_stream) if gate_stream else None))
             self._gate = gate
+
+    def _gate_check(self):
+        # a failed device-gate store surfaces here (the transitions return void, channel.hpp)
+        if self._gate is not None:
+            self._b.check(self._b.lib.valve_channel_gate_status(self._h))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -615,18 +624,23 @@ class ChannelController:
 
     def note_busy(self, t: int) -> None:
         self._b.fn("channel_note_busy")(self._h, int(t))
+        self._gate_check()
 
     def note_all_idle(self, t: int) -> None:
         self._b.fn("channel_note_all_idle")(self._h, int(t))
 
     def ensure_disabled(self, t: int) -> int:
-        return self._b.fn("channel_ensure_disabled")(self._h, int(t))
+        e = self._b.fn("channel_ensure_disabled")(self._h, int(t))
+        self._gate_check()
+        return e
 
     def handle_toggle(self, t: int, gen: int) -> None:
         self._b.fn("channel_handle_toggle")(self._h, int(t), int(gen))
+        self._gate_check()
 
     def handle_cooldown(self, t: int, gen: int) -> None:
         self._b.fn("channel_handle_cooldown")(self._h, int(t), int(gen))
+        self._gate_check()
 
 
 # ----------------------------------------------------------- device-only (B200) surfaces
@@ -711,6 +725,8 @@ def _declare_valve_extras(L):
         "valve_offline_reset": (C.c_int, [vp]),
         "valve_offline_gemm": (C.c_int, [vp, P(OfflineGemmWork), vp]),
         "valve_channel_bind_gate": (C.c_int, [vp, vp]),
+        "valve_channel_bind_gate_stream": (C.c_int, [vp, vp, vp]),
+        "valve_channel_gate_status": (C.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kNT)
   const int nblk0 = row >= 0 ? P.row_nblk[row] : 0;
   if (threadIdx.x == 0) {
     if ((int64_t)nblk0 + pages > P.P) {
-      set_err(P, kErrRuntime, kDetBlocksFull, P.P);
+      set_err(P, kErrRuntime, kDetBlocksFull, (int64_t)nblk0 + pages);  // the row length needed
       s_fail = 1;
     } else if (row < 0) {
       s_row = ht_insert(P, req);
@@ -195,6 +195,20 @@ __global__ void __launch_bounds__(kNT)
     P.mirror->r[0] = 1;
   }
   publish(P);
+}
+
+// Request-hash rebuild after a table growth (valve_host.cu grow_tables): every live row of the
+// old table is inserted into P's (empty, larger) table with CAS probing.
+__global__ void k_ht_rehash(PoolDev P, const int* old_row, int old_hc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= old_hc) return;
+  const int row = old_row[i];
+  if (row < 0) return;
+  const int64_t key = P.row_req[row];
+  const int mask = P.HC - 1;
+  int j = ht_slot(key, P.HC);
+  while (atomicCAS(&P.ht_row[j], kEmpty, row) != kEmpty) j = (j + 1) & mask;
+  P.ht_key[j] = key;
 }
 
 __global__ void __launch_bounds__(kNT) k_offline_release(PoolDev P, int64_t req) {
@@ -439,7 +453,11 @@ __global__ void k_set_costs(PoolDev P, int n, const int64_t* reqs, const int64_t
 
 // tile prefix of the offline work list: prefix[i] = sum_{j<i} npages[j] * chunks_per_page
 __global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix,
-                              unsigned long long* total_out) {
+                              unsigned long long* total_out, unsigned* frozen) {
+  // the work list is frozen from the first launch after a reset (valve_offline_reset clears
+  // the flag): resumed launches -- direct or replays of a captured graph -- keep the prefix the
+  // saved cursors refer to
+  if (frozen && *(volatile unsigned*)frozen) return;
   __shared__ long long s_carry;
   if (threadIdx.x == 0) s_carry = 0;
   __syncthreads();
@@ -456,6 +474,7 @@ __global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix
   if (threadIdx.x == 0) {
     prefix[n] = s_carry * (int64_t)cpp;
     if (total_out) *total_out = (unsigned long long)(s_carry * (int64_t)cpp);
+    if (frozen) *frozen = 1u;
   }
 }
 

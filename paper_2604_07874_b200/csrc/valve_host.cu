@@ -245,7 +245,7 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
     fail(VALVE_INVALID_ARGUMENT, "MemoryPool: handle_size_pages > 256 is not supported on device");
   if ((int64_t)c.total_handles * c.handle_size_pages >= (1 << 24))
     fail(VALVE_INVALID_ARGUMENT, "MemoryPool: total pages must be < 2^24");
-  if (c.max_requests <= 0 || c.max_requests >= (1 << 16) || c.max_pages_per_request <= 0)
+  if (c.max_requests <= 0 || c.max_requests >= (1 << 24) || c.max_pages_per_request <= 0)
     fail(VALVE_INVALID_ARGUMENT, "MemoryPool: bad request-table geometry");
   if (c.slot_bytes < 0 || c.page_bytes < 0 || c.page_bytes > c.slot_bytes || c.page_bytes % 16 ||
       c.slot_bytes % 16)
@@ -375,6 +375,120 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
 
 namespace {
 
+// Replaces a pool array by a larger one; `keep` leading elements are copied, the rest is
+// filled with `fill` bytes (or left uninitialised for scratch when fill < 0).
+template <class T>
+void regrow(valve_pool* p, T*& ptr, int64_t keep, int64_t n, int fill) {
+  void* np = nullptr;
+  ck(cudaMalloc(&np, std::max<int64_t>(n, 1) * sizeof(T)), "cudaMalloc(table growth)");
+  if (fill >= 0) ck(cudaMemsetAsync(np, fill, n * sizeof(T), p->stream), "memset");
+  if (keep > 0) ck(cudaMemcpyAsync(np, ptr, keep * sizeof(T), cudaMemcpyDeviceToDevice, p->stream), "copy");
+  ck(cudaStreamSynchronize(p->stream), "table growth");
+  auto it = std::find(p->dev_allocs.begin(), p->dev_allocs.end(), static_cast<void*>(ptr));
+  if (it != p->dev_allocs.end()) *it = np;
+  cudaFree(ptr);
+  ptr = static_cast<T*>(np);
+}
+
+// Grows the device request table to R2 rows of P2 blocks.  The reference MemoryPool has no
+// limit on live requests or pages per request (memory.hpp:81-97 std::map / std::vector); the
+// device tables start small (apply and reserve scan them) and grow on demand, so a drop-in
+// caller never sees a capacity error the reference would not raise.  Row ids, the free-row
+// FIFO order, block tables and the last reclaim report are preserved; the request hash is
+// rebuilt at its new capacity.
+void grow_tables(valve_pool* p, int R2, int P2) {
+  const int R = p->R, P = p->Pblk;
+  R2 = std::max(R2, R);
+  P2 = std::max(P2, P);
+  if (R2 == R && P2 == P) return;
+  if (R2 >= (1 << 24)) fail(VALVE_RUNTIME_ERROR, "MemoryPool: request table beyond 2^24 rows");
+  for (cudaStream_t s : {p->plan_stream, p->copy_stream, p->stream})
+    ck(cudaStreamSynchronize(s), "table growth");
+  PoolDev& d = p->d;
+  const int64_t HS = (int64_t)p->H * p->S;
+  if (P2 != P || R2 != R) {  // block tables: new pitch and/or more rows
+    int* nbt = nullptr;
+    ck(cudaMalloc((void**)&nbt, (size_t)R2 * P2 * 4), "cudaMalloc(block tables)");
+    ck(cudaMemsetAsync(nbt, 0xff, (size_t)R2 * P2 * 4, p->stream), "memset");
+    ck(cudaMemcpy2DAsync(nbt, (size_t)P2 * 4, d.bt, (size_t)P * 4, (size_t)P * 4, R, cudaMemcpyDeviceToDevice,
+                         p->stream), "copy");
+    ck(cudaStreamSynchronize(p->stream), "table growth");
+    auto it = std::find(p->dev_allocs.begin(), p->dev_allocs.end(), static_cast<void*>(d.bt));
+    if (it != p->dev_allocs.end()) *it = nbt;
+    cudaFree(d.bt);
+    d.bt = nbt;
+  }
+  if (P2 != P) regrow(p, p->d_ids, 0, std::max<int64_t>(std::max(p->H, 1) * 2, P2), -1);
+  if (R2 != R) {
+    // free-row FIFO: the live window [head, tail) in order, then the new rows
+    PoolHdr hdr;
+    ck(cudaMemcpy(&hdr, d.hdr, sizeof hdr, cudaMemcpyDeviceToHost), "read");
+    std::vector<int> ring(R), nring;
+    ck(cudaMemcpy(ring.data(), d.ring, (size_t)R * 4, cudaMemcpyDeviceToHost), "read");
+    for (int i = hdr.ring_head; i < hdr.ring_tail; ++i) nring.push_back(ring[i % R]);
+    for (int r = R; r < R2; ++r) nring.push_back(r);
+    regrow(p, d.ring, 0, R2, -1);
+    ck(cudaMemcpy(d.ring, nring.data(), nring.size() * 4, cudaMemcpyHostToDevice), "upload");
+    hdr.ring_head = 0;
+    hdr.ring_tail = (int)nring.size();
+    hdr.tombstones = 0;
+    // state rows (kept) and per-row scratch (fresh)
+    regrow(p, d.row_req, R, R2, 0);
+    regrow(p, d.row_cost, R, R2, 0);
+    regrow(p, d.row_pbytes, R, R2, 0);
+    regrow(p, d.row_npages, R, R2, 0);
+    regrow(p, d.row_nblk, R, R2, 0);
+    regrow(p, d.s_ev, 0, R2, 0);
+    regrow(p, d.s_qoff, 0, R2 + 1, -1);
+    regrow(p, d.s_qcnt, 0, std::max<int64_t>(HS, R2), -1);
+    regrow(p, d.s_evrows, 0, R2, -1);
+    regrow(p, d.s_rank, 0, R2, -1);
+    regrow(p, d.res_evicted, R, R2, 0);
+    regrow(p, d.res_inv_off, R + 1, R2 + 1, 0);
+    regrow(p, d.res_ev_pbytes, R, R2, 0);
+    regrow(p, d.res_ev_base, R + 1, R2 + 1, 0);
+    regrow(p, d.res_ev_cbase, R + 1, R2 + 1, 0);
+    regrow(p, p->d_in64, 0, R2, -1);
+    regrow(p, p->d_in64b, 0, R2, -1);
+    for (auto& c : p->cs) {
+      regrow(p, c.inv_off, 0, R2 + 1, -1);
+      regrow(p, c.ev_pbytes, 0, R2, -1);
+      regrow(p, c.ev_base, 0, R2 + 1, -1);
+      regrow(p, c.ev_cbase, 0, R2 + 1, -1);
+    }
+    // request hash at its new capacity: re-insert every live row
+    const int HC2 = (int)next_pow2(2 * (int64_t)R2);
+    int* old_row = d.ht_row;
+    int64_t* old_key = d.ht_key;
+    const int HC = d.HC;
+    int* nrow = nullptr;
+    int64_t* nkey = nullptr;
+    ck(cudaMalloc((void**)&nrow, (size_t)HC2 * 4), "cudaMalloc(request hash)");
+    ck(cudaMalloc((void**)&nkey, (size_t)HC2 * 8), "cudaMalloc(request hash)");
+    ck(cudaMemsetAsync(nrow, 0xff, (size_t)HC2 * 4, p->stream), "memset");
+    d.ht_row = nrow;
+    d.ht_key = nkey;
+    d.HC = HC2;
+    d.R = R2;
+    p->R = R2;
+    ck(cudaMemcpyAsync(d.hdr, &hdr, sizeof hdr, cudaMemcpyHostToDevice, p->stream), "upload");
+    k_ht_rehash<<<(HC + 255) / 256, 256, 0, p->stream>>>(d, old_row, HC);
+    counted();
+    ck(cudaGetLastError(), "rehash launch");
+    ck(cudaStreamSynchronize(p->stream), "rehash");
+    for (void*& a : p->dev_allocs) {
+      if (a == old_row) a = nrow;
+      else if (a == old_key) a = nkey;
+    }
+    cudaFree(old_row);
+    cudaFree(old_key);
+  }
+  d.P = P2;
+  p->Pblk = P2;
+  p->cfg.max_requests = p->R;
+  p->cfg.max_pages_per_request = P2;
+}
+
 void read_apply_results(valve_pool* p, int* handles, int64_t* evicted, int* inv_off, int64_t* pages,
                         int* phys, int* blk, int cap_h, int cap_ev, int cap_pages) {
   const int nh = p->last_n_handles, ne = p->last_n_evicted, np = p->last_n_pages;
@@ -484,7 +598,24 @@ int valve_pool_offline_reserve(valve_pool* p, int64_t req, int pages, int64_t t,
       *ok = 1;
       return;
     }
-    p->launch1("offline_reserve", k_offline_reserve, 0, p->d, req, pages, t, max_off);
+    // The kernel checks table capacity before it mutates anything: on a full table, grow it
+    // and run the reservation again (the reference has no such limit).
+    const int64_t HS = (int64_t)p->H * p->S;
+    for (int attempt = 0;; ++attempt) {
+      try {
+        p->launch1("offline_reserve", k_offline_reserve, 0, p->d, req, pages, t, max_off);
+        break;
+      } catch (const Err&) {
+        const int det = p->mirror->err_detail;
+        if (attempt >= 4 || (det != kDetRowsFull && det != kDetBlocksFull)) throw;
+        p->mirror->err = 0;
+        if (det == kDetRowsFull)
+          grow_tables(p, (int)std::min<int64_t>(2 * (int64_t)p->R, std::max<int64_t>(HS, p->R + 1)), p->Pblk);
+        else
+          grow_tables(p, p->R, (int)std::min<int64_t>(std::max<int64_t>(2 * (int64_t)p->Pblk, p->mirror->err_arg),
+                                                       std::max<int64_t>(HS, p->mirror->err_arg)));
+      }
+    }
     *ok = (int)p->mirror->r[0];
   });
 }
@@ -1185,9 +1316,12 @@ int valve_evicted_cost(int device, int n, const int* ids, const int* off, const 
     SelectCtx& C = select_ctx(device);
     std::lock_guard<std::mutex> lk(C.mu);
     ck(cudaSetDevice(device), "cudaSetDevice");
+    if (n < 0 || m < 0 || n_pick < 0) fail(VALVE_INVALID_ARGUMENT, "evicted_cost: negative sizes");
+    // size every buffer (the pick list may be longer than the instance: duplicates and unknown
+    // ids are legal input, reclaim.cpp:19-31) BEFORE the upload -- growing afterwards would free
+    // buffers the uploaded SelectArgs still point at
+    C.reserve(std::max(n, n_pick), n ? off[n] : 0, m);
     SelectArgs A = upload_instance(C, n, ids, nullptr, off, reqs, m, keys, vals, 0, 0);
-    C.reserve(n, n ? off[n] : 0, std::max(m, n_pick));
-    if (n_pick > C.cap_n) C.reserve(n_pick, 0, 0);
     if (n_pick)
       ck(cudaMemcpyAsync(C.pick, pick, (size_t)n_pick * 4, cudaMemcpyHostToDevice, C.stream), "upload");
     A.ev = C.ev;
@@ -1295,6 +1429,14 @@ struct valve_gate {
   std::vector<cudaStream_t> wait_streams;
   std::vector<cudaEvent_t> wait_events;
   int fanout_mode = VALVE_FANOUT_BATCHED;
+  // The decode work list (tile prefix over the listed rows) is frozen by the first launch after
+  // valve_offline_reset: resumed launches reuse it, so the striped cursors (the context save)
+  // keep meaning the same tiles even when reclaims / re-admissions change the pool's rows.
+  std::vector<void*> retired;  // replaced prefix buffers (freed with the gate)
+  bool frozen = false;
+  const int* frozen_rows = nullptr;
+  int frozen_n = 0;
+  int64_t frozen_chunk = 0;
   ~valve_gate() {
     if (stream) cudaStreamSynchronize(stream);
     if (work_stream) {
@@ -1306,6 +1448,7 @@ struct valve_gate {
     if (d && remote) cudaIpcCloseMemHandle(d);
     else if (d) cudaFree(d);
     if (d_prefix) cudaFree(d_prefix);
+    for (void* r : retired) cudaFree(r);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -1442,7 +1585,6 @@ int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* s) {
       ck(cudaStreamWaitEvent(ws, g->wait_events[2 * i], 0), "event wait");
       cu_ck(op.wait32((CUstream)ws, dptr(&g->peers[i]->d->live_ctas), 0, CU_STREAM_WAIT_VALUE_EQ),
             "cuStreamWaitValue32");
-      cu_ck(op.write32((CUstream)ws, dptr(&g->peers[i]->d->quiesced_gen), gen, 0), "cuStreamWriteValue32");
       ck(cudaEventRecord(g->wait_events[2 * i + 1], ws), "event");
     }
     cu_ck(op.wait32((CUstream)st, dptr(&g->d->live_ctas), 0, CU_STREAM_WAIT_VALUE_EQ), "cuStreamWaitValue32");
@@ -1554,7 +1696,9 @@ int valve_offline_reset(valve_gate* g) {
     ck(cudaSetDevice(g->device), "cudaSetDevice");
     ck(cudaMemsetAsync(&g->d->t_first_seen, 0, 4 * sizeof(unsigned long long), g->stream), "memset");
     ck(cudaMemsetAsync(g->d->cursor, 0, sizeof(g->d->cursor), g->stream), "memset");
+    ck(cudaMemsetAsync(&g->d->frozen, 0, sizeof(unsigned), g->stream), "memset");
     ck(cudaStreamSynchronize(g->stream), "reset");
+    g->frozen = false;
   });
 }
 
@@ -1572,12 +1716,25 @@ int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work*
     const int64_t chunk = w->tile_bytes > 0 ? w->tile_bytes : 16384;
     if (chunk % 16) fail(VALVE_INVALID_ARGUMENT, "offline_launch: tile_bytes must be a 16-byte multiple");
     const int cpp = (int)((p->d.page_bytes + chunk - 1) / chunk);
-    if (n_req + 1 > g->cap_prefix) {
-      if (g->d_prefix) cudaFree(g->d_prefix);
-      g->cap_prefix = std::max<int64_t>(n_req + 1, 2 * g->cap_prefix);
-      ck(cudaMalloc((void**)&g->d_prefix, g->cap_prefix * 8), "cudaMalloc");
+    if (!g->frozen) {
+      if (n_req + 1 > g->cap_prefix) {
+        // an earlier launch may still read the old prefix (possibly queued behind a closed
+        // gate): retire it to the gate's lifetime instead of freeing it now
+        if (g->d_prefix) g->retired.push_back(g->d_prefix);
+        g->cap_prefix = std::max<int64_t>(n_req + 1, 2 * g->cap_prefix);
+        ck(cudaMalloc((void**)&g->d_prefix, g->cap_prefix * 8), "cudaMalloc");
+      }
+      g->frozen = true;
+      g->frozen_rows = w->rows;
+      g->frozen_n = n_req;
+      g->frozen_chunk = chunk;
+    } else if (g->frozen_rows != w->rows || g->frozen_n != n_req || g->frozen_chunk != chunk) {
+      fail(VALVE_LOGIC_ERROR,
+           "offline_launch: resumed with another work list (call valve_offline_reset for new work)");
     }
-    k_tile_prefix<<<1, kNT, 0, st>>>(npages, n_req, cpp, g->d_prefix, &g->d->total);
+    // always enqueued (a no-op on the device once the list is frozen), so a captured launch
+    // sequence freezes its list on the first replay after a reset, like a direct launch
+    k_tile_prefix<<<1, kNT, 0, st>>>(npages, n_req, cpp, g->d_prefix, &g->d->total, &g->d->frozen);
     counted();
     int threads = w->threads > 0 ? w->threads : 256;
     int ctas = w->ctas;
@@ -1729,13 +1886,24 @@ struct valve_channel {
   void log(int64_t t, int what, int64_t aux, int mem) {
     if (h.log) h.log(h.user, t, what, aux, mem);
   }
-  int gate_status = VALVE_OK;  // last device-gate store (the C hooks return void)
+  // First failed device-gate store since the last valve_channel_gate_status() (the state
+  // machine's entry points return void, like the reference's): sticky, so a failed raise is
+  // never lost between two edges.
+  int gate_status = VALVE_OK;
+  std::string gate_err;
+  void gate_store(int rc) {
+    if (rc != VALVE_OK && gate_status == VALVE_OK) {
+      gate_status = rc;
+      gate_err = g_err;
+    }
+  }
   void gate_raise() {
-    if (gate) gate_status = valve_gate_raise(gate, (uint32_t)gen, nullptr);
+    if (gate) gate_store(valve_gate_raise(gate, (uint32_t)gen, gate_stream));
   }
   void gate_release() {
-    if (gate) gate_status = valve_gate_release(gate, (uint32_t)gen, nullptr);
+    if (gate) gate_store(valve_gate_release(gate, (uint32_t)gen, gate_stream));
   }
+  void* gate_stream = nullptr;  // stream the gate stores are issued on (NULL: the gate's own)
   void issue_disable(int64_t t, bool mem) {
     // channel.cpp:13-20; the device gate closes at issue (offline stops at its next tile)
     state = 1;
@@ -1774,6 +1942,18 @@ void valve_channel_destroy(valve_channel* c) { delete c; }
 int valve_channel_bind_gate(valve_channel* c, valve_gate* g) {
   c->gate = g;
   return VALVE_OK;
+}
+int valve_channel_bind_gate_stream(valve_channel* c, valve_gate* g, void* stream) {
+  c->gate = g;
+  c->gate_stream = stream;
+  return VALVE_OK;
+}
+int valve_channel_gate_status(valve_channel* c) {
+  const int rc = c->gate_status;
+  if (rc != VALVE_OK) g_err = "ChannelController: device gate store failed: " + c->gate_err;
+  c->gate_status = VALVE_OK;
+  c->gate_err.clear();
+  return rc;
 }
 int valve_channel_state(const valve_channel* c) { return c->state; }
 int valve_channel_offline_compute_allowed(const valve_channel* c) { return c->state == 0; }

@@ -29,6 +29,7 @@ __global__ void k_online_grow(PoolDev P, int k, int64_t t);
 __global__ void k_online_release(PoolDev P, int k, int64_t online_used);
 __global__ void k_offline_reserve(PoolDev P, int64_t req, int pages, int64_t t, int max_off);
 __global__ void k_offline_release(PoolDev P, int64_t req);
+__global__ void k_ht_rehash(PoolDev P, const int* old_row, int old_hc);
 __global__ void k_requests_on_handle(PoolDev P, int h, int64_t* out);
 __global__ void k_handles_of_request(PoolDev P, int64_t req, int* out);
 __global__ void k_offline_pages_of(PoolDev P, int64_t req);
@@ -44,7 +45,7 @@ __global__ void k_set_costs(PoolDev P, int n, const int64_t* reqs, const int64_t
 __global__ void k_select_instance(SelectArgs A);
 __global__ void k_map_refs(const int64_t* reqs, int nnz, const int64_t* keys, int m, int* rref);
 __global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix,
-                              unsigned long long* total_out);
+                              unsigned long long* total_out, unsigned* frozen);
 __global__ void k_evicted_cost(SelectArgs A, const int* pick, int n_pick);
 extern __device__ long long g_greedy_cycles[2];
 extern __device__ long long g_apply_ns[6];
@@ -107,6 +108,8 @@ struct GateDev {
   unsigned long long cursor[kStripes];    // per-stripe claims (the context save)
   unsigned long long t_raise;             // %globaltimer of a kernel-issued raise (diagnostic)
   unsigned long long stripes;             // cursors the current work list uses (0 = kStripes)
+  unsigned int frozen;                    // decode work list (tile prefix) fixed since the reset
+  unsigned int pad_;
 };
 __global__ void k_gate_raise_stamp(GateDev* g, unsigned gen);
 struct OfflineArgs {

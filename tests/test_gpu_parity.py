@@ -284,3 +284,43 @@ def test_device_errors_match_reference(ref):
         assert pool.online_handles() == 1  # first conversion stuck (memory.cpp mutates in order)
     with pytest.raises(A.InvalidArgument):
         A.MemoryPool(0, 4, 16)
+
+
+# ------------------------------------------------------------- round-2 boundary regressions
+
+def test_evicted_cost_long_pick_lists_device_vs_reference(ref):
+    """Pick lists longer than the instance -- duplicates and unknown ids, which the reference
+    accepts (reclaim.cpp:19-31) -- once made the device path grow its buffers after the instance
+    upload (use-after-free).  Device vs the reference itself, sized past every buffer's capacity."""
+    rng = random.Random(4242)
+    for _ in range(120):
+        inst = fuzz.random_instance(rng, n_max=rng.choice([1, 3, 12]), cost_max=rng.choice([5, 10**9]))
+        ids = [h.id for h in inst.handles]
+        n_pick = rng.choice([len(ids) + 1, 2 * len(ids) + 3, 64, 257])
+        pick = [rng.choice(ids) for _ in range(n_pick)]
+        if rng.random() < 0.3:
+            pick[rng.randrange(n_pick)] = max(ids) + 1000  # unknown id -> invalid_argument
+        a = fuzz.outcome(lambda: A.evicted_cost(inst, pick, backend=ref))
+        b = fuzz.outcome(lambda: A.evicted_cost(inst, pick))
+        assert a == b, (inst, pick)
+
+
+@pytest.mark.parametrize("seed,geom,rows,blocks", [
+    (0, (16, 4), 1, 1), (1, (32, 8), 2, 4), (2, (64, 16), 3, 8), (3, (12, 64), 1, 16),
+])
+def test_request_table_grows_like_the_reference(oracle_c, seed, geom, rows, blocks):
+    """The device request table starts at `rows` x `blocks` and must grow on demand: the
+    reference MemoryPool has no limit on live requests or pages per request.  The
+    randomized sequence (with block tables and physical pages compared) forces several growths
+    of both dimensions mid-run, interleaved with reclaims."""
+    rng = random.Random(9000 + seed)
+    H, S = geom
+    pair = fuzz.PoolPair(H, S, 16, None, oracle_c, extended=True)
+    pair.a = A.MemoryPool(H, S, 16, config=dict(max_requests=rows, max_pages_per_request=blocks))
+    fuzz.random_pool_ops(pair, rng, 400)
+    # one request spanning the whole pool
+    pair.call("online_release", H)
+    big = 10**6
+    pair.call("offline_reserve", big, pair.a.free_handles() * S, 5000, -1)
+    pair.call("block_table", big)
+    pair.call("check_invariants")

@@ -138,6 +138,8 @@ typedef struct {
   double rate_bytes_per_s;  /* rate bound; <= 0 = unbounded */
   int64_t burst_bytes;      /* token-bucket depth for the rate bound */
   int use_tma;              /* 1 = stage chunks through shared memory with cp.async.bulk */
+  void* trace;              /* optional device uint64[n_chunks]: %globaltimer issue time of each
+                               chunk (rate-bound tests); NULL = off */
 } valve_copy_params;
 typedef struct {
   int64_t bytes;
@@ -161,6 +163,23 @@ int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
 int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_bytes,
                                   const valve_copy_params* params);
 int valve_pool_reclaim_copy_wait(valve_pool* p, valve_copy_stats* stats);
+/* Rate bound (rate_bytes_per_s, burst_bytes): a token bucket whose state lives in the pool, so it
+ * bounds bytes per window ACROSS copies: in any interval of length w the pool's copies start at
+ * most rate*w + burst + one chunk of bytes (back-to-back pipelined ops share one budget). */
+
+/* Landed tickets -- when may a reclaimed slot be rewritten (SURVEY §7 hard part 2)?  Every copy
+ * publishes "waves" to one monotone pool counter as it reads them out of HBM.  With a uniform
+ * page size the SM kernel runs wave-major: wave w = bytes [w*wave_bytes, (w+1)*wave_bytes) of
+ * EVERY page of the report, so an online tenant writing its KV layer by layer into reclaimed
+ * slots waits only for the waves under the bytes it is about to write, not for the whole op.
+ * (Other paths publish the copy as one wave covering the slot.)  Copy i's waves are numbered
+ * wave_base .. wave_base + n_waves - 1; ticket t is out once the counter is >= t. */
+int valve_pool_copy_ticket(const valve_pool* p, uint64_t* wave_base, int* n_waves, int64_t* wave_bytes);
+/* Makes `stream` (NULL: the pool stream) wait (cuStreamWaitValue64 GEQ) until `ticket` waves
+ * have been published.  Takes no SM. */
+int valve_pool_wait_landed(valve_pool* p, uint64_t ticket, void* stream);
+/* Current published count and the total issued so far (diagnostics / host polling). */
+int valve_pool_landed(const valve_pool* p, uint64_t* landed, uint64_t* issued);
 /* Restore (scatter) of host-resident pages into a live request's slots: host page i (of
  * n_pages, page_bytes each, pinned/mapped) is written to block blk_of_page[i] of `req` -- the
  * inverse of the gather, e.g. offline weight pages evicted to host by a reclaim (C3) and

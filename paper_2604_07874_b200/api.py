@@ -653,7 +653,8 @@ class PoolConfig(C.Structure):
 
 class CopyParams(C.Structure):
     _fields_ = [("ctas", C.c_int), ("threads", C.c_int), ("chunk_bytes", i64),
-                ("rate_bytes_per_s", dbl), ("burst_bytes", i64), ("use_tma", C.c_int)]
+                ("rate_bytes_per_s", dbl), ("burst_bytes", i64), ("use_tma", C.c_int),
+                ("trace", C.c_void_p)]
 
 
 class CopyStats(C.Structure):
@@ -700,6 +701,9 @@ def _declare_valve_extras(L):
         "valve_pool_reclaim_copy_ce": (C.c_int, [vp, vp, i64, P(CopyStats)]),
         "valve_pool_reclaim_copy_start": (C.c_int, [vp, vp, i64, P(CopyParams)]),
         "valve_pool_reclaim_copy_wait": (C.c_int, [vp, P(CopyStats)]),
+        "valve_pool_copy_ticket": (C.c_int, [vp, P(C.c_uint64), P(C.c_int), P(i64)]),
+        "valve_pool_wait_landed": (C.c_int, [vp, C.c_uint64, vp]),
+        "valve_pool_landed": (C.c_int, [vp, P(C.c_uint64), P(C.c_uint64)]),
         "valve_pool_reclaim_phases": (C.c_int, [vp, P(i64)]),
         "valve_pool_restore": (C.c_int, [vp, i64, vp, C.c_int, P(C.c_int), P(CopyParams), P(CopyStats)]),
         "valve_pool_set_page_bytes": (C.c_int, [vp, C.c_int, P(i64), P(i64)]),
@@ -827,6 +831,25 @@ class DevicePool(MemoryPool):
         st = CopyStats()
         self._b.check(self._b.lib.valve_pool_reclaim_copy_wait(self._h, C.byref(st)))
         return st
+
+    def copy_ticket(self):
+        """(wave_base, n_waves, wave_bytes) of the last started copy: wave w of it covers slot
+        bytes [w*wave_bytes, (w+1)*wave_bytes) of every reclaimed page and is out once
+        landed() >= wave_base + w + 1 (valve_pool_copy_ticket)."""
+        b, n, wb = C.c_uint64(0), C.c_int(0), C.c_int64(0)
+        self._b.check(self._b.lib.valve_pool_copy_ticket(self._h, C.byref(b), C.byref(n), C.byref(wb)))
+        return b.value, n.value, wb.value
+
+    def wait_landed(self, ticket: int, stream: Optional[int] = None):
+        """Stream-ordered wait (cuStreamWaitValue64 >=) for `ticket` published copy waves."""
+        self._b.check(self._b.lib.valve_pool_wait_landed(self._h, int(ticket),
+                                                         C.c_void_p(stream) if stream else None))
+
+    def landed(self):
+        """(published waves, issued waves)."""
+        a, b = C.c_uint64(0), C.c_uint64(0)
+        self._b.check(self._b.lib.valve_pool_landed(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def restore(self, req: int, host_ptr: int, blocks: Sequence[int],
                 params: Optional[CopyParams] = None) -> CopyStats:

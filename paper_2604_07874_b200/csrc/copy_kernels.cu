@@ -6,8 +6,9 @@
 // CTAs stream the whole list while the rest of the GPU stays with online work.  Each thread
 // keeps kVec 16-byte loads in flight (ld.global.nc.L1::no_allocate -- the pool is read once),
 // then issues 16-byte stores to the host-mapped destination (posted PCIe writes).  The rate
-// bound is a token bucket on %globaltimer: chunk c may start once
-//   now >= t0 + (c*chunk - burst) * ns_per_byte.
+// bound is a GCRA token bucket on %globaltimer whose state (the theoretical arrival time) lives
+// in the pool, so it holds across copy launches: in any window of length w the copies issue at
+// most rate * w + burst + one chunk bytes.
 // No UVM: the destination is cudaHostAlloc'd / registered memory, never managed memory.
 #include "valve_kernels.h"
 
@@ -29,18 +30,49 @@ __device__ __forceinline__ void st_host(uint4* p, const uint4& v) {
                : "memory");
 }
 
-__device__ __forceinline__ unsigned long long start_time(unsigned long long* t_first) {
-  const unsigned long long now = globaltimer_ns();
-  const unsigned long long prev = atomicCAS(t_first, 0ull, now);
-  return prev ? prev : now;
+__device__ __forceinline__ void start_time(unsigned long long* t_first) {
+  atomicCAS(t_first, 0ull, globaltimer_ns());
 }
 
-__device__ __forceinline__ void pace(const CopyArgs& A, unsigned long long t0, long long c) {
-  if (A.ns_per_byte <= 0.0) return;
-  const double credit = (double)(c * A.chunk_bytes - A.burst_bytes) * A.ns_per_byte;
-  if (credit <= 0.0) return;
-  const unsigned long long allowed = t0 + (unsigned long long)credit;
-  while (globaltimer_ns() < allowed) __nanosleep(2000);
+// GCRA pacing of one chunk of `bytes`: reserve [s, s + bytes * ns_per_byte) on the pool's
+// virtual timeline, s = max(tat, now - burst_ns), and start at s.  Consecutive reservations
+// never overlap, and s >= now - burst_ns, so chunks starting inside any window [a, b] have
+// s in [a - burst_ns, b]: at most (b - a) * rate + burst + one chunk bytes.
+__device__ __forceinline__ void pace(const CopyArgs& A, int64_t bytes, long long c) {
+  if (A.ns_per_byte > 0.0) {
+    const unsigned long long cost = (unsigned long long)((double)bytes * A.ns_per_byte);
+    const unsigned long long now = globaltimer_ns();
+    const unsigned long long burst = (unsigned long long)A.burst_ns;
+    const unsigned long long floor = now > burst ? now - burst : 0ull;
+    unsigned long long old = *(volatile unsigned long long*)A.tat, s;
+    for (;;) {
+      s = old > floor ? old : floor;
+      const unsigned long long prev = atomicCAS(A.tat, old, s + cost);
+      if (prev == old) break;
+      old = prev;
+    }
+    while (globaltimer_ns() < s) __nanosleep(1000);
+  }
+  if (A.trace) A.trace[c] = globaltimer_ns();
+}
+
+// Publishes every completed wave in order (any thread may call; CAS hands each wave to one).
+__device__ __forceinline__ void publish_waves(const CopyArgs& A, unsigned per_wave) {
+  __threadfence();  // this chunk's count before the read of wave_next (store-buffer pattern)
+  for (;;) {
+    const unsigned w = *(volatile unsigned*)A.wave_next;
+    if (w >= (unsigned)A.n_waves) break;
+    if (*(volatile unsigned*)&A.wave_done[w] < per_wave) break;
+    if (atomicCAS(A.wave_next, w, w + 1) == w) atomicMax(A.landed, A.wave_base + w + 1);
+    __threadfence();
+  }
+}
+
+// Last CTA out publishes the whole copy (paths without per-wave publication, and a backstop).
+__device__ __forceinline__ void publish_all(const CopyArgs& A) {
+  __threadfence();
+  if (atomicAdd(A.ctas_done, 1u) == gridDim.x - 1 && A.n_waves > 0)
+    atomicMax(A.landed, A.wave_base + (unsigned long long)A.n_waves);
 }
 
 }  // namespace
@@ -65,17 +97,22 @@ __global__ void k_copy_plan(const int64_t* ev_pbytes, const int* inv_off, int n_
 
 __global__ void __launch_bounds__(512) k_reclaim_copy(CopyArgs A) {
   __shared__ long long s_chunk;
-  __shared__ unsigned long long s_t0;
   __shared__ int64_t s_src, s_dst, s_len;
-  if (threadIdx.x == 0) s_t0 = start_time(A.t_first);
+  if (threadIdx.x == 0) start_time(A.t_first);
   const int64_t cpp = (A.page_bytes + A.chunk_bytes - 1) / A.chunk_bytes;
   const long long n_chunks = A.ev_cbase ? A.ev_cbase[A.n_ev] : A.n_chunks;
+  long long prev = -1;  // thread 0: the chunk this CTA finished last (its wave is counted next)
   for (;;) {
+    if (A.wave_major) __syncthreads();  // every thread's loads of chunk `prev` have returned
     if (threadIdx.x == 0) {
+      if (prev >= 0 && A.wave_major) {
+        const unsigned w = (unsigned)(prev / A.n_pages);
+        if (atomicAdd(&A.wave_done[w], 1u) + 1u == (unsigned)A.n_pages) publish_waves(A, (unsigned)A.n_pages);
+      }
       const long long c = (long long)atomicAdd(A.cursor, 1ull);
       s_chunk = c;
+      prev = c;
       if (c < n_chunks) {
-        pace(A, s_t0, c);
         if (A.ev_cbase) {  // variable page sizes: locate the evicted request by its chunk prefix
           int lo = 0, hi = A.n_ev - 1;
           while (lo < hi) {
@@ -91,11 +128,19 @@ __global__ void __launch_bounds__(512) k_reclaim_copy(CopyArgs A) {
           s_dst = A.ev_base[lo] + pg * pb + off;
           s_len = min(A.chunk_bytes, pb - off);
         } else {
-          const int64_t page = c / cpp, off = (c % cpp) * A.chunk_bytes;
+          int64_t page, off;
+          if (A.wave_major) {
+            page = c % A.n_pages;
+            off = (c / A.n_pages) * A.chunk_bytes;
+          } else {
+            page = c / cpp;
+            off = (c % cpp) * A.chunk_bytes;
+          }
           s_src = (int64_t)A.phys[page] * A.slot_bytes + off;
           s_dst = page * A.page_bytes + off;
           s_len = min(A.chunk_bytes, A.page_bytes - off);
         }
+        pace(A, s_len, c);
       }
     }
     __syncthreads();
@@ -124,7 +169,10 @@ __global__ void __launch_bounds__(512) k_reclaim_copy(CopyArgs A) {
   // stores retired system-wide before the completion stamp
   __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) atomicMax(A.t_last, globaltimer_ns());
+  if (threadIdx.x == 0) {
+    atomicMax(A.t_last, globaltimer_ns());
+    publish_all(A);
+  }
 }
 
 // Variant staging each chunk through shared memory with the bulk-copy engine:
@@ -182,7 +230,7 @@ __global__ void __launch_bounds__(32) k_reclaim_copy_tma(CopyArgs A) {
   extern __shared__ __align__(128) unsigned char sbuf[];  // 2 x kTmaChunk
   __shared__ __align__(8) uint64_t bar[2];
   if (threadIdx.x != 0) return;
-  const unsigned long long t0 = start_time(A.t_first);
+  start_time(A.t_first);
   mbar_init(&bar[0], 1);
   mbar_init(&bar[1], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -192,10 +240,10 @@ __global__ void __launch_bounds__(32) k_reclaim_copy_tma(CopyArgs A) {
   for (;;) {
     const long long c = (long long)atomicAdd(A.cursor, 1ull);
     if (c >= A.n_chunks) break;
-    pace(A, t0, c);
     const int64_t page = c / cpp;
     const int64_t off0 = (c % cpp) * A.chunk_bytes;
     const int64_t len = min(A.chunk_bytes, A.page_bytes - off0);
+    pace(A, len, c);
     const uint8_t* src = A.pages + (int64_t)A.phys[page] * A.slot_bytes + off0;
     uint8_t* dst = A.dst + page * A.page_bytes + off0;
     for (int64_t o = 0; o < len; o += kTmaChunk) {
@@ -213,6 +261,7 @@ __global__ void __launch_bounds__(32) k_reclaim_copy_tma(CopyArgs A) {
   bulk_wait_all();
   __threadfence_system();
   atomicMax(A.t_last, globaltimer_ns());
+  publish_all(A);
 }
 
 // Scatter of host-resident pages back into HBM (the restore side of a reclaim that copied,

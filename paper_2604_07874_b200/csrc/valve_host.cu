@@ -59,11 +59,13 @@ void counted() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 using PFN_write32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 using PFN_wait32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 using PFN_write64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+using PFN_wait64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 using PFN_batch = CUresult (*)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
 struct MemOps {
   PFN_write32 write32 = nullptr;
   PFN_wait32 wait32 = nullptr;
   PFN_write64 write64 = nullptr;
+  PFN_wait64 wait64 = nullptr;
   PFN_batch batch = nullptr;
 };
 const MemOps& memops() {
@@ -74,15 +76,18 @@ const MemOps& memops() {
     cudaGetDriverEntryPoint("cuStreamWriteValue32", (void**)&ops.write32, cudaEnableDefault, &q);
     cudaGetDriverEntryPoint("cuStreamWaitValue32", (void**)&ops.wait32, cudaEnableDefault, &q);
     cudaGetDriverEntryPoint("cuStreamWriteValue64", (void**)&ops.write64, cudaEnableDefault, &q);
+    cudaGetDriverEntryPoint("cuStreamWaitValue64", (void**)&ops.wait64, cudaEnableDefault, &q);
     cudaGetDriverEntryPoint("cuStreamBatchMemOp", (void**)&ops.batch, cudaEnableDefault, &q);
   });
-  if (!ops.write32 || !ops.wait32 || !ops.write64 || !ops.batch)
+  if (!ops.write32 || !ops.wait32 || !ops.write64 || !ops.wait64 || !ops.batch)
     fail(VALVE_CUDA_ERROR, "stream memory operations unavailable in this driver");
   return ops;
 }
 void cu_ck(CUresult r, const char* what) {
   if (r != CUDA_SUCCESS) fail(VALVE_CUDA_ERROR, std::string(what) + " failed (CUresult " + std::to_string((int)r) + ")");
 }
+
+CUdeviceptr dptr(const void* p) { return reinterpret_cast<CUdeviceptr>(p); }
 
 int64_t next_pow2(int64_t n) {
   int64_t p = 1;
@@ -141,9 +146,17 @@ struct valve_pool {
     int64_t* ev_base = nullptr;
     int64_t* ev_cbase = nullptr;
     unsigned long long* ctr = nullptr;  // cursor, t_first, t_last
+    unsigned* waves = nullptr;          // [kMaxWaves] per-wave done counts, then next, ctas_done
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_plan = nullptr;
     int64_t bytes = 0, pages = 0;
+    uint64_t wave_base = 0;
+    int n_waves = 0;
+    int64_t wave_bytes = 0;
   };
+  static constexpr int kMaxWaves = 1024;
+  unsigned long long* d_landed = nullptr;  // published copy waves (monotone, all copies)
+  unsigned long long* d_tat = nullptr;     // rate bound: GCRA theoretical arrival time (ns)
+  uint64_t waves_issued = 0;               // sum of n_waves over started copies
   static constexpr int kCopySlots = 2;
   CopySlot cs[kCopySlots];
   int cs_head = 0, cs_n = 0, cs_last = -1;
@@ -324,6 +337,10 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   p->d_in64 = p->dalloc<int64_t>(R);
   p->d_in64b = p->dalloc<int64_t>(R);
   p->d_copyctr = p->dalloc<unsigned long long>(4);
+  p->d_landed = p->dalloc<unsigned long long>(1);
+  p->d_tat = p->dalloc<unsigned long long>(1);
+  ck(cudaMemsetAsync(p->d_landed, 0, 8, p->stream), "memset");
+  ck(cudaMemsetAsync(p->d_tat, 0, 8, p->stream), "memset");
   for (auto& cs : p->cs) {
     cs.phys = p->dalloc<int>(HS);
     cs.inv_off = p->dalloc<int>(R + 1);
@@ -331,6 +348,7 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
     cs.ev_base = p->dalloc<int64_t>(R + 1);
     cs.ev_cbase = p->dalloc<int64_t>(R + 1);
     cs.ctr = p->dalloc<unsigned long long>(4);
+    cs.waves = p->dalloc<unsigned>(valve_pool::kMaxWaves + 2);
     ck(cudaEventCreate(&cs.ev0), "cudaEventCreate");
     ck(cudaEventCreate(&cs.ev1), "cudaEventCreate");
     ck(cudaEventCreateWithFlags(&cs.ev_plan, cudaEventDisableTiming), "cudaEventCreate");
@@ -887,6 +905,7 @@ void valve_copy_params_default(valve_copy_params* c) {
   c->rate_bytes_per_s = 0;
   c->burst_bytes = 0;
   c->use_tma = 0;
+  c->trace = nullptr;
 }
 
 int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_bytes,
@@ -927,9 +946,22 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
     A.dst = static_cast<uint8_t*>(ddst);
     A.ns_per_byte = c.rate_bytes_per_s > 0 ? 1e9 / c.rate_bytes_per_s : 0.0;
     A.burst_bytes = c.burst_bytes;
+    A.burst_ns = (double)std::max<int64_t>(c.burst_bytes, 0) * A.ns_per_byte;
+    A.tat = p->d_tat;
+    A.trace = static_cast<unsigned long long*>(c.trace);
     A.cursor = S.ctr;
     A.t_first = S.ctr + 1;
     A.t_last = S.ctr + 2;
+    // landed tickets: wave-major order (one wave = the same chunk_bytes of every page) when the
+    // page size is uniform and the SM kernel runs; otherwise the whole copy is one wave
+    A.wave_major = (!custom && !c.use_tma && cpp <= valve_pool::kMaxWaves && n_pages > 0) ? 1 : 0;
+    A.n_waves = n_pages == 0 ? 0 : (A.wave_major ? (int)cpp : 1);
+    A.wave_done = S.waves;
+    A.wave_next = S.waves + valve_pool::kMaxWaves;
+    A.ctas_done = S.waves + valve_pool::kMaxWaves + 1;
+    A.landed = p->d_landed;
+    A.wave_base = p->waves_issued;
+    if (c.trace && c.use_tma) fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: trace needs the SM copy kernel");
     // the copy runs on its own stream after the report exists and works from its own snapshot
     // of it; bookkeeping and the next decision proceed on the pool stream meanwhile
     // the snapshot runs on the plan stream, so a copy queued behind a running one does not hold
@@ -946,6 +978,7 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
     ck(cudaEventRecord(S.ev_plan, p->plan_stream), "event");
     ck(cudaStreamWaitEvent(p->copy_stream, S.ev_plan, 0), "event wait");
     ck(cudaMemsetAsync(S.ctr, 0, 24, p->copy_stream), "memset");
+    ck(cudaMemsetAsync(S.waves, 0, (valve_pool::kMaxWaves + 2) * sizeof(unsigned), p->copy_stream), "memset");
     if (custom) {  // per-request page sizes: chunk prefix over the evicted requests first
       A.ev_pbytes = S.ev_pbytes;
       A.ev_base = S.ev_base;
@@ -971,6 +1004,10 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
     ck(cudaGetLastError(), "reclaim_copy launch");
     S.bytes = need;
     S.pages = n_pages;
+    S.wave_base = A.wave_base;
+    S.n_waves = A.n_waves;
+    S.wave_bytes = A.wave_major ? c.chunk_bytes : p->d.slot_bytes;
+    p->waves_issued += (uint64_t)A.n_waves;
     p->cs_n++;
     p->cs_last = si;
   });
@@ -995,6 +1032,39 @@ int valve_pool_reclaim_copy_wait(valve_pool* p, valve_copy_stats* st) {
       st->t_first_ns = t[1];
       st->t_last_ns = t[2];
     }
+  });
+}
+
+int valve_pool_copy_ticket(const valve_pool* p, uint64_t* wave_base, int* n_waves, int64_t* wave_bytes) {
+  return guard([&] {
+    if (p->cs_last < 0) fail(VALVE_LOGIC_ERROR, "copy_ticket: no reclaim copy was started");
+    const valve_pool::CopySlot& S = p->cs[p->cs_last];
+    if (wave_base) *wave_base = S.wave_base;
+    if (n_waves) *n_waves = S.n_waves;
+    if (wave_bytes) *wave_bytes = S.wave_bytes;
+  });
+}
+
+int valve_pool_wait_landed(valve_pool* p, uint64_t target, void* stream) {
+  return guard([&] {
+    const MemOps& op = memops();
+    if (target > p->waves_issued)
+      fail(VALVE_INVALID_ARGUMENT, "wait_landed: ticket beyond the waves of the copies started");
+    if (target == 0) return;
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    cu_ck(op.wait64((CUstream)(stream ? static_cast<cudaStream_t>(stream) : p->stream), dptr(p->d_landed),
+                    (cuuint64_t)target, CU_STREAM_WAIT_VALUE_GEQ),
+          "cuStreamWaitValue64");
+  });
+}
+
+int valve_pool_landed(const valve_pool* p, uint64_t* landed, uint64_t* issued) {
+  return guard([&] {
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    unsigned long long v = 0;
+    ck(cudaMemcpy(&v, p->d_landed, 8, cudaMemcpyDeviceToHost), "read");
+    if (landed) *landed = v;
+    if (issued) *issued = p->waves_issued;
   });
 }
 
@@ -1455,7 +1525,6 @@ struct valve_gate {
 
 namespace {
 cudaStream_t as_stream(void* s, cudaStream_t dflt) { return s ? static_cast<cudaStream_t>(s) : dflt; }
-CUdeviceptr dptr(const void* p) { return reinterpret_cast<CUdeviceptr>(p); }
 
 // One submission of stream memory operations (executed in array order by the front end).
 struct MemBatch {

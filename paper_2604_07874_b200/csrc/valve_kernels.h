@@ -69,6 +69,23 @@ struct CopyArgs {
   const int64_t* ev_cbase;   // chunk prefix per evicted request [n_ev + 1]
   const int* inv_off;        // first report page of each evicted request
   int n_ev;
+  // Wave-major order (uniform page size): chunk c covers byte range wave*chunk of page
+  // c % n_pages, wave = c / n_pages, so wave w holds the same slot bytes of every page.  Once
+  // every chunk of wave w has been read from HBM the kernel publishes wave_base + w + 1 to the
+  // pool-global, monotone `landed` word, in wave order: an online write into a reclaimed slot
+  // may proceed (cuStreamWaitValue64 >= ticket) once the waves covering its bytes are out.
+  int wave_major;
+  int n_waves;                   // waves this copy publishes (0: no chunks)
+  unsigned* wave_done;           // [n_waves] chunks read per wave
+  unsigned* wave_next;           // next wave to publish
+  unsigned* ctas_done;           // CTAs finished (the last one publishes everything)
+  unsigned long long* landed;    // pool-global published-wave counter
+  unsigned long long wave_base;  // global index of this copy's wave 0
+  // Rate bound across launches: a GCRA token bucket whose theoretical arrival time (ns) lives
+  // in the pool, so back-to-back copies share one budget of rate * window + burst bytes.
+  unsigned long long* tat;
+  double burst_ns;
+  unsigned long long* trace;     // optional [n_chunks]: issue time of each chunk (tests)
 };
 __global__ void k_reclaim_copy(CopyArgs A);
 __global__ void k_copy_plan(const int64_t* ev_pbytes, const int* inv_off, int n_ev, int64_t chunk,

@@ -128,7 +128,8 @@ def test_rate_bound_holds_per_window_across_copies(oracle_c):
         worst = max(worst, float(excess.max()))
     # %globaltimer granularity and the sleep loop: allow one more chunk of slack
     assert worst <= chunk, worst
-    # the second copy started without a fresh burst: its first chunks are paced right away
+    # the second copy got no fresh burst (a per-launch bucket would issue its first burst/chunk
+    # chunks at once): only the credit of the short gap between the two kernels is left
     t2 = np.sort(traces[1].cpu().numpy().astype(np.int64))
-    t1_end = np.sort(traces[0].cpu().numpy().astype(np.int64))[-1]
-    assert (t2[: burst // chunk] >= t1_end - 2 * burst * ns_per_byte).all()
+    m = burst // chunk
+    assert t2[m - 1] - t2[0] >= 0.5 * (m - 1) * chunk * ns_per_byte, (t2[:m] - t2[0])

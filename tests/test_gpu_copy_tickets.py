@@ -44,15 +44,23 @@ def test_tickets_guard_every_wave_against_online_overwrites(oracle_c):
                         device="cuda", dtype=torch.long)
     buf = A.HostBuffer(n_pages * pool.page_bytes)
     chunk = 8192
-    # slow enough (0.5 GB/s) that an early overwrite would certainly beat the copy
+    slots = _slot_tensor(torch, pool)
+    assert slots.data_ptr() == pool.view().pages  # a view of the page store, not a copy
+    online = torch.cuda.Stream()
+    with torch.cuda.stream(online):  # first-use costs outside the race below
+        pool.wait_landed(0, online.cuda_stream)
+        slots[phys[:1], 0:16] = slots[phys[:1], 0:16]
+        torch.cuda.Event(enable_timing=True).record(online)
+    online.synchronize()
+    # slow enough (0.1 GB/s, ~24 ms) that an early overwrite would certainly beat the copy
     pool.reclaim_copy_start(buf.ptr, buf.nbytes, A.copy_params(ctas=3, chunk_bytes=chunk,
-                                                                 rate_bytes_per_s=5e8, burst_bytes=chunk))
+                                                                 rate_bytes_per_s=1e8, burst_bytes=chunk))
     base, waves, wave_bytes = pool.copy_ticket()
     assert waves == -(-pool.page_bytes // chunk) and wave_bytes == chunk
-    slots = _slot_tensor(torch, pool)
-    online = torch.cuda.Stream()
     events = []
     with torch.cuda.stream(online):
+        e_start = torch.cuda.Event(enable_timing=True)
+        e_start.record(online)
         for w in range(waves):
             pool.wait_landed(base + w + 1, online.cuda_stream)
             lo, hi = w * chunk, min((w + 1) * chunk, pool.page_bytes)
@@ -65,9 +73,11 @@ def test_tickets_guard_every_wave_against_online_overwrites(oracle_c):
     assert np.array_equal(buf.view(), want), "a wave was published before its bytes were read"
     landed, issued = pool.landed()
     assert landed == issued == base + waves
-    # the waves were released progressively, not all at the end of the copy
-    t_first = events[0].elapsed_time(events[-1])
-    assert t_first > 0.3 * st.kernel_ms, (t_first, st.kernel_ms)
+    # the overwrites really landed in the page store, wave after wave over the copy's duration
+    assert bool((slots[phys, :pool.page_bytes] == 0xA5).all())
+    rel = [e_start.elapsed_time(e) for e in events]
+    assert rel[0] < 0.5 * st.kernel_ms and rel[-1] > 0.7 * st.kernel_ms, (rel, st.kernel_ms)
+    assert all(b > a for a, b in zip(rel, rel[1:])), rel
 
 
 def test_tickets_accumulate_across_pipelined_copies(oracle_c):
@@ -104,19 +114,24 @@ def test_rate_bound_holds_per_window_across_copies(oracle_c):
     rng = random.Random(7)
     pool, live = _pool_with_pages(rng, H=64, S=8, slot=65536, page=65536, n_req=110)
     rate, burst, chunk = 2e9, 256 << 10, 16384
-    traces, sizes = [], []
-    bufs = []
+    k = 6
+    cap = k * pool.handle_size_pages()  # pages per op at most
+    # everything allocated up front (cudaHostAlloc blocks for ms): the second copy is queued
+    # right behind the first, so the two share the bucket with no idle gap between them
+    bufs = [A.HostBuffer(cap * pool.page_bytes) for _ in range(2)]
+    traces = [torch.zeros(cap * (pool.page_bytes // chunk), dtype=torch.int64, device="cuda") for _ in range(2)]
+    torch.cuda.synchronize()
+    ns = []
     for op in range(2):
-        _, _, n = pool.reclaim(6, 1000 + op)
-        tr = torch.zeros(n * (pool.page_bytes // chunk), dtype=torch.int64, device="cuda")
-        b = A.HostBuffer(n * pool.page_bytes)
-        bufs.append(b)
-        pool.reclaim_copy_start(b.ptr, b.nbytes, A.copy_params(ctas=4, chunk_bytes=chunk, rate_bytes_per_s=rate,
-                                                                 burst_bytes=burst, trace=tr.data_ptr()))
-        traces.append(tr)
+        _, _, n = pool.reclaim(k, 1000 + op)
+        ns.append(n * (pool.page_bytes // chunk))
+        pool.reclaim_copy_start(bufs[op].ptr, bufs[op].nbytes,
+                                A.copy_params(ctas=4, chunk_bytes=chunk, rate_bytes_per_s=rate, burst_bytes=burst,
+                                              trace=traces[op].data_ptr()))
     for _ in range(2):
         pool.reclaim_copy_wait()
-    t = np.sort(torch.cat(traces).cpu().numpy().astype(np.int64))
+    tr = [traces[i][: ns[i]].cpu().numpy().astype(np.int64) for i in range(2)]
+    t = np.sort(np.concatenate(tr))
     assert t.size > 100 and (t > 0).all()
     ns_per_byte = 1e9 / rate
     # bytes started in [t_i, t_j] vs the budget, for every pair (two-pointer over the sorted trace)
@@ -128,8 +143,9 @@ def test_rate_bound_holds_per_window_across_copies(oracle_c):
         worst = max(worst, float(excess.max()))
     # %globaltimer granularity and the sleep loop: allow one more chunk of slack
     assert worst <= chunk, worst
-    # the second copy got no fresh burst (a per-launch bucket would issue its first burst/chunk
-    # chunks at once): only the credit of the short gap between the two kernels is left
-    t2 = np.sort(traces[1].cpu().numpy().astype(np.int64))
+    # the second copy started right behind the first and got no fresh burst (a per-launch bucket
+    # would start its first burst/chunk chunks at once)
+    t1, t2 = np.sort(tr[0]), np.sort(tr[1])
     m = burst // chunk
+    assert t2[0] - t1[-1] < 0.25 * burst * ns_per_byte, (t2[0] - t1[-1])
     assert t2[m - 1] - t2[0] >= 0.5 * (m - 1) * chunk * ns_per_byte, (t2[:m] - t2[0])

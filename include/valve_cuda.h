@@ -66,6 +66,13 @@ void valve_pool_config_default(valve_pool_config* cfg);
 int valve_pool_create(int total_handles, int handle_size_pages, int page_size_tokens, valve_pool** out);
 int valve_pool_create_ex(const valve_pool_config* cfg, valve_pool** out);
 void valve_pool_destroy(valve_pool* p);
+/* Back to the freshly created state (all handles free, empty request table, no copies, idle rate
+ * bucket), keeping the allocation and the page store's bytes.  Waits for in-flight copies. */
+int valve_pool_reset(valve_pool* p);
+/* Ids of the online-reserved handles, ascending (the physical home of online pages: the
+ * reference keeps online pages as an aggregate, memory.hpp:97, so a tenant that places its KV
+ * in the pool's slots needs to know which handles it holds). */
+int valve_pool_online_handles(const valve_pool* p, int* out, int cap, int* n);
 
 /* out = {free_handles, online_handles, offline_handles, online_used_pages,
  *        online_capacity_pages}  (memory.hpp:28-41) */
@@ -257,6 +264,7 @@ typedef struct {
   uint64_t canary_hits;    /* reads that resolved to the quarantine page */
   uint64_t tiles_claimed;  /* tiles handed out by the HBM stripe cursors (the context save) */
   uint64_t t_raise_ns;     /* %globaltimer of the last valve_gate_raise_stamped() */
+  uint64_t total_tiles;    /* tiles of the current (frozen) work list */
 } valve_gate_state;
 int valve_gate_create(int device, valve_gate** out);
 void valve_gate_destroy(valve_gate* g);
@@ -309,6 +317,10 @@ int valve_offline_launch(valve_gate* g, valve_pool* p, const valve_offline_work*
  * blocks then read as quarantine / unmapped and count as canary hits).  Resuming with another
  * rows / n_requests / tile_bytes without a reset is a VALVE_LOGIC_ERROR. */
 int valve_offline_reset(valve_gate* g);
+/* Drops what is left of the current work list: every queued or later resumed launch (decode pass
+ * or GEMM, also one still waiting for an open gate) claims nothing and retires at once.  For
+ * shutting a tenant down behind a closed gate without running its remaining tiles. */
+int valve_offline_cancel(valve_gate* g);
 
 /* Gated offline GEMM: C = A * B^T in bf16 with fp32 accumulation on the tcgen05
  * tensor cores (TMA-fed, TMEM accumulator), persistent over 128 x 256 tiles of C claimed from

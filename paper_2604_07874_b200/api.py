@@ -666,7 +666,7 @@ class GateState(C.Structure):
     _fields_ = [("gen", u32), ("closed", u32), ("quiesced_gen", u32), ("live_ctas", u32),
                 ("t_first_seen_ns", C.c_uint64), ("t_quiesced_ns", C.c_uint64),
                 ("tiles_done", C.c_uint64), ("canary_hits", C.c_uint64),
-                ("tiles_claimed", C.c_uint64), ("t_raise_ns", C.c_uint64)]
+                ("tiles_claimed", C.c_uint64), ("t_raise_ns", C.c_uint64), ("total_tiles", C.c_uint64)]
 
 
 class OfflineWork(C.Structure):
@@ -701,6 +701,8 @@ def _declare_valve_extras(L):
         "valve_pool_reclaim_copy_ce": (C.c_int, [vp, vp, i64, P(CopyStats)]),
         "valve_pool_reclaim_copy_start": (C.c_int, [vp, vp, i64, P(CopyParams)]),
         "valve_pool_reclaim_copy_wait": (C.c_int, [vp, P(CopyStats)]),
+        "valve_pool_reset": (C.c_int, [vp]),
+        "valve_pool_online_handles": (C.c_int, [vp, P(C.c_int), C.c_int, P(C.c_int)]),
         "valve_pool_copy_ticket": (C.c_int, [vp, P(C.c_uint64), P(C.c_int), P(i64)]),
         "valve_pool_wait_landed": (C.c_int, [vp, C.c_uint64, vp]),
         "valve_pool_landed": (C.c_int, [vp, P(C.c_uint64), P(C.c_uint64)]),
@@ -727,6 +729,7 @@ def _declare_valve_extras(L):
         "valve_gate_stream": (vp, [vp]),
         "valve_offline_launch": (C.c_int, [vp, vp, P(OfflineWork), vp]),
         "valve_offline_reset": (C.c_int, [vp]),
+        "valve_offline_cancel": (C.c_int, [vp]),
         "valve_offline_gemm": (C.c_int, [vp, P(OfflineGemmWork), vp]),
         "valve_channel_bind_gate": (C.c_int, [vp, vp]),
         "valve_channel_bind_gate_stream": (C.c_int, [vp, vp, vp]),
@@ -831,6 +834,17 @@ class DevicePool(MemoryPool):
         st = CopyStats()
         self._b.check(self._b.lib.valve_pool_reclaim_copy_wait(self._h, C.byref(st)))
         return st
+
+    def reset(self) -> None:
+        """Back to the freshly created state, keeping the allocation (valve_pool_reset)."""
+        self._b.check(self._b.lib.valve_pool_reset(self._h))
+        self._last = (0, 0, 0)
+
+    def online_handle_ids(self) -> List[int]:
+        """Online-reserved handle ids, ascending (valve_pool_online_handles)."""
+        out, n = _arr(C.c_int, self._total), C.c_int(0)
+        self._b.check(self._b.lib.valve_pool_online_handles(self._h, _ptr(out, C.c_int), self._total, C.byref(n)))
+        return [out[i] for i in range(n.value)]
 
     def copy_ticket(self):
         """(wave_base, n_waves, wave_bytes) of the last started copy: wave w of it covers slot
@@ -988,6 +1002,10 @@ class Gate:
 
     def reset_work(self):
         self._b.check(self._b.lib.valve_offline_reset(self._h))
+
+    def cancel_work(self):
+        """Drop the rest of the work list: queued / resumed launches retire at once."""
+        self._b.check(self._b.lib.valve_offline_cancel(self._h))
 
     def launch_gemm(self, a_ptr: int, b_ptr: int, c_ptr: int, m: int, n: int, k: int, *, ctas: int = 0,
                     poll: bool = True, stream: Optional[int] = None, fresh: bool = False, mode: int = 0):

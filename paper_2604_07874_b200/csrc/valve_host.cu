@@ -251,6 +251,8 @@ static void set_reclaim_smem_attrs() {
      "cudaFuncSetAttribute");
 }
 
+static void pool_reset_state(valve_pool* p);
+
 static void pool_init(valve_pool* p, const valve_pool_config& c) {
   if (c.total_handles <= 0 || c.handle_size_pages <= 0 || c.page_size_tokens <= 0)
     fail(VALVE_INVALID_ARGUMENT, "MemoryPool: sizes must be > 0");  // memory.cpp:15
@@ -339,8 +341,6 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   p->d_copyctr = p->dalloc<unsigned long long>(4);
   p->d_landed = p->dalloc<unsigned long long>(1);
   p->d_tat = p->dalloc<unsigned long long>(1);
-  ck(cudaMemsetAsync(p->d_landed, 0, 8, p->stream), "memset");
-  ck(cudaMemsetAsync(p->d_tat, 0, 8, p->stream), "memset");
   for (auto& cs : p->cs) {
     cs.phys = p->dalloc<int>(HS);
     cs.inv_off = p->dalloc<int>(R + 1);
@@ -361,9 +361,22 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
     d.pages = static_cast<uint8_t*>(pg);
   }
   ck(cudaHostAlloc((void**)&p->mirror, sizeof(Mirror), cudaHostAllocMapped), "cudaHostAlloc");
-  std::memset(p->mirror, 0, sizeof(Mirror));
   ck(cudaHostGetDevicePointer((void**)&d.mirror, p->mirror, 0), "cudaHostGetDevicePointer");
-  // initial state: all handles free, no slots, empty request table, every row in the ring
+  pool_reset_state(p);
+  // dynamic shared memory: greedy marginals (2048 handles) aliased with the apply sort
+  // buffers (8192 x {u64 key, i32 block})
+  p->smem_snapshot = 0;
+  p->smem_reclaim = kReclaimSmemBytes;
+  set_reclaim_smem_attrs();
+}
+
+// Initial state: all handles free, no slots, empty request table, every row in the ring, no
+// copies published, an idle rate bucket.  (The page store keeps its bytes.)
+static void pool_reset_state(valve_pool* p) {
+  PoolDev& d = p->d;
+  const int H = p->H, S = p->S, R = p->R;
+  const int64_t HS = (int64_t)H * S;
+  std::memset(p->mirror, 0, sizeof(Mirror));
   ck(cudaMemsetAsync(d.hstate, 0, H, p->stream), "memset");
   ck(cudaMemsetAsync(d.hmapped, 0, H * 8, p->stream), "memset");
   ck(cudaMemsetAsync(d.hused, 0, H * 4, p->stream), "memset");
@@ -382,13 +395,17 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   ck(cudaMemcpyAsync(d.ring, ring.data(), R * 4, cudaMemcpyHostToDevice, p->stream), "upload");
   PoolHdr hdr{H, 0, 0, 0, R, 0};
   ck(cudaMemcpyAsync(d.hdr, &hdr, sizeof hdr, cudaMemcpyHostToDevice, p->stream), "upload");
+  ck(cudaMemsetAsync(p->d_landed, 0, 8, p->stream), "memset");
+  ck(cudaMemsetAsync(p->d_tat, 0, 8, p->stream), "memset");
   ck(cudaStreamSynchronize(p->stream), "init");
   p->mirror->n_free = H;
-  // dynamic shared memory: greedy marginals (2048 handles) aliased with the apply sort
-  // buffers (8192 x {u64 key, i32 block})
-  p->smem_snapshot = 0;
-  p->smem_reclaim = kReclaimSmemBytes;
-  set_reclaim_smem_attrs();
+  p->online_used = 0;
+  p->waves_issued = 0;
+  p->last_n_handles = p->last_n_evicted = p->last_n_pages = 0;
+  p->last_copy_bytes = 0;
+  p->last_custom = 0;
+  p->cs_head = p->cs_n = 0;
+  p->cs_last = -1;
 }
 
 namespace {
@@ -561,6 +578,31 @@ int valve_pool_create(int H, int S, int T, valve_pool** out) {
 }
 
 void valve_pool_destroy(valve_pool* p) { delete p; }
+
+int valve_pool_reset(valve_pool* p) {
+  return guard([&] {
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    for (cudaStream_t s : {p->plan_stream, p->copy_stream, p->stream}) ck(cudaStreamSynchronize(s), "reset");
+    pool_reset_state(p);
+  });
+}
+
+int valve_pool_online_handles(const valve_pool* cp, int* out, int cap, int* n) {
+  auto* p = const_cast<valve_pool*>(cp);
+  return guard([&] {
+    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+    std::vector<uint8_t> st(p->H);
+    ck(cudaMemcpyAsync(st.data(), p->d.hstate, p->H, cudaMemcpyDeviceToHost, p->stream), "read");
+    ck(cudaStreamSynchronize(p->stream), "read");
+    int k = 0;
+    for (int h = 0; h < p->H; ++h)
+      if (st[h] == kOnline) {
+        if (out && k < cap) out[k] = h;
+        ++k;
+      }
+    *n = k;
+  });
+}
 
 int valve_pool_counts(const valve_pool* p, int64_t out[5]) {
   p->counts(out);
@@ -1757,6 +1799,7 @@ int valve_gate_read(const valve_gate* g, valve_gate_state* o) {
     }
     o->tiles_claimed = claimed;
     o->t_raise_ns = h.t_raise;
+    o->total_tiles = h.total;
   });
 }
 
@@ -1768,6 +1811,16 @@ int valve_offline_reset(valve_gate* g) {
     ck(cudaMemsetAsync(&g->d->frozen, 0, sizeof(unsigned), g->stream), "memset");
     ck(cudaStreamSynchronize(g->stream), "reset");
     g->frozen = false;
+  });
+}
+
+int valve_offline_cancel(valve_gate* g) {
+  return guard([&] {
+    if (g->remote) fail(VALVE_LOGIC_ERROR, "offline_cancel: remote gate");
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    // saturated cursors: every stripe reads as exhausted (the kernels compare before claiming)
+    ck(cudaMemsetAsync(g->d->cursor, 0x7f, sizeof(g->d->cursor), g->stream), "memset");
+    ck(cudaStreamSynchronize(g->stream), "cancel");
   });
 }
 

@@ -431,13 +431,15 @@ class OffReq:
 
 class OfflineEngine:
     """Request-level offline engine driven by the harvested GPU work (sim.cpp:730-858): FIFO
-    admission into the pool (resumed requests first), prefill of recompute_cost() forwards, then
-    batched decode (one forward per request per token, max_offline_batch 256); completion frees
-    the pages.  Evictions (the invalidation callback, sim.cpp:994-1050) drop the request's
+    admission into the pool (resumed requests first), prefill of recompute_cost() forwards in
+    chunks interleaved with batched decode steps (one forward per request per token,
+    max_offline_batch 256); completion frees the pages.  Evictions (the invalidation callback, sim.cpp:994-1050) drop the request's
     progress: it re-prefills input + generated tokens after re-admission."""
 
-    def __init__(self, pool: A.DevicePool, backlog, log: EventLog, page_tokens=PAGE_TOKENS, max_batch=256):
+    def __init__(self, pool: A.DevicePool, backlog, log: EventLog, page_tokens=PAGE_TOKENS, max_batch=256,
+                 chunk=2048):
         self.pool, self.log = pool, log
+        self.chunk = chunk
         self.page_tokens = page_tokens
         self.max_batch = max_batch
         self.reqs = {rid: OffReq(rid, i, o) for rid, i, o in backlog}
@@ -481,44 +483,50 @@ class OfflineEngine:
         return {r.rid: r.recompute_cost() for r in self.live()}
 
     def advance(self, forwards: float, now: int, horizon_us: int):
-        """Spend harvested token-forwards: prefill first (FIFO), then decode iterations."""
+        """Spend harvested token-forwards, iteration by iteration as a continuous-batching engine
+        does: one decode step of the running batch (one forward per request), then a prefill
+        chunk of up to `chunk` forwards of the FIFO head(s).  Returns whether pages were freed."""
         self.forwards += forwards
         f = int(forwards + self.carry)
         self.carry = forwards + self.carry - f
         freed = False
         while f > 0:
-            if self.prefill_q:
+            progressed = False
+            batch = self.decoding[: self.max_batch]
+            if batch and f >= len(batch):
+                f -= len(batch)
+                progressed = True
+                for rid in batch:
+                    r = self.reqs[rid]
+                    r.generated += 1
+                    r.invested += 1
+                    if r.generated == r.output:
+                        r.state = "done"
+                        self.decoding.remove(rid)
+                        self.pool.offline_release(rid)
+                        freed = True
+                        if now <= horizon_us:
+                            self.tokens_done += r.generated
+                            self.completed += 1
+                            self.log.add(now, "done", **{"class": "offline"}, request_id=rid, gpu=0,
+                                         tokens=r.generated, first_token_us=-1, last_token_us=-1,
+                                         digest="0x0000000000000000")
+            budget = min(f, self.chunk)
+            while budget > 0 and self.prefill_q:
                 r = self.reqs[self.prefill_q[0]]
-                use = min(f, r.prefill_left)
+                use = min(budget, r.prefill_left)
                 r.prefill_left -= use
                 r.invested += use
+                budget -= use
                 f -= use
+                progressed = True
                 if r.prefill_left == 0:
                     self.prefill_q.popleft()
                     r.state = "decode"
                     self.decoding.append(r.rid)
-                continue
-            if not self.decoding:
-                break
-            batch = self.decoding[: self.max_batch]
-            if f < len(batch):
+            if not progressed:
                 self.carry += f
                 break
-            f -= len(batch)
-            for rid in batch:
-                r = self.reqs[rid]
-                r.generated += 1
-                r.invested += 1
-                if r.generated == r.output:
-                    r.state = "done"
-                    self.decoding.remove(rid)
-                    self.pool.offline_release(rid)
-                    freed = True
-                    if now <= horizon_us:
-                        self.tokens_done += r.generated
-                        self.completed += 1
-                        self.log.add(now, "done", **{"class": "offline"}, request_id=rid, gpu=0, tokens=r.generated,
-                                     first_token_us=-1, last_token_us=-1, digest="0x0000000000000000")
         return freed
 
     def on_evicted(self, rids, now: int, kill: bool):
@@ -571,6 +579,7 @@ class RunResult:
     shortfall_to_write_us: List[float] = field(default_factory=list)   # reclaim issued -> first layer write allowed
     shortfall_full_copy_us: List[float] = field(default_factory=list)  # reclaim issued -> whole copy out
     decision_us: List[float] = field(default_factory=list)
+    op_phase_us: Dict[str, float] = field(default_factory=dict)
     decode_iter_us: List[float] = field(default_factory=list)
     prefill_us: List[float] = field(default_factory=list)
     log: EventLog = field(default_factory=EventLog)
@@ -822,17 +831,23 @@ class Colocation:
         rate-bounded gather copy of the invalidated pages, whose slots carry the copy's ticket."""
         op = self.res.reclaims
         self.res.log.add(now, "reclaim_request", gpu=0, handles=int(k), op=op, purpose=purpose)
+        ph = self.res.op_phase_us
         t0 = time.perf_counter()
         self._harvest(now, force=True)
         if self.offline.live():
             self.pool.set_costs(self.offline.costs())
+        t1 = time.perf_counter()
         self._quiesce_order_pool(now)
         mode = 1 if (kill or self.policy == "valve-fifo") else 0
         old_h = self.pool.online_handles()
         td = time.perf_counter()
         nh, ne, npg = self.pool.reclaim(k, now, mode)
-        self.res.decision_us.append((time.perf_counter() - td) * 1e6)
+        t3 = time.perf_counter()
+        self.res.decision_us.append((t3 - td) * 1e6)
         res = self.pool.last_reclaim()
+        t4 = time.perf_counter()
+        for key, a_, b_ in (("costs", t0, t1), ("order", t1, td), ("decision", td, t3), ("result", t3, t4)):
+            ph[key] = ph.get(key, 0.0) + (b_ - a_) * 1e6
         if self.cfg.copy and not kill and npg:
             if len(self._copies) == 2:
                 self._complete_copy()
@@ -857,8 +872,12 @@ class Colocation:
                 self.pool.wait_landed(base + n, self.observer.cuda_stream)
                 e2.record(self.observer)
                 self._shortfall_marks.append((t0, e1, e2))
+        t5 = time.perf_counter()
         self.pages.sync_handles()
-        lat = int((time.perf_counter() - t0) * 1e6)
+        t6 = time.perf_counter()
+        ph["copy_start"] = ph.get("copy_start", 0.0) + (t5 - t4) * 1e6
+        ph["sync_handles"] = ph.get("sync_handles", 0.0) + (t6 - t5) * 1e6
+        lat = int((t6 - t0) * 1e6)
         self.res.log.add(now, "reclaim_done", gpu=0, op=op, latency_us=lat, handle_ids=list(res.handles))
         self.res.log.add(now, "reserve_change", gpu=0, old_handles=old_h, new_handles=self.pool.online_handles(),
                          cause="pressure" if purpose == "growth" else "demand")
@@ -1064,13 +1083,22 @@ class Colocation:
                     act = ("decode", len(decoding))
                 finished = act is None and nxt >= len(reqs)
             else:
+                # exact replay: the planned prefill goes after exactly the recorded number of decode
+                # iterations; if its request has not arrived yet the loop waits for it (spinning
+                # while a batch is decoding: the lane stays busy), so both arms of a pair run the
+                # same batches in the same order and differ only in step durations
                 finished = pi >= len(plan) and not decoding
-                if pi < len(plan):
-                    rid, k = plan[pi]
-                    if by_rid[rid].arrival_us <= now and (n_decodes >= k or not decoding):
+                spin = False
+                if pi < len(plan) and (n_decodes >= plan[pi][1] or not decoding):
+                    rid = plan[pi][0]
+                    if by_rid[rid].arrival_us <= now:
                         act = ("prefill", rid)
-                if act is None and decoding:
+                    elif decoding:
+                        spin = True
+                elif decoding:
                     act = ("decode", len(decoding))
+                if spin:
+                    continue
             # page demand of the action (sim.cpp:469-511); a policy that cannot supply it stalls
             need, need_by = 0, []
             if act is not None:
@@ -1426,6 +1454,7 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
             "pressure_events": r.pressure, "stalls": r.stalls,
             "copy_gb": r.copy_bytes / 1e9, "copy_gbs_mean": (sum(r.copy_gbs) / len(r.copy_gbs)) if r.copy_gbs else None,
             "decision_us_p50": _pct([d for x in rs for d in x.decision_us], 50),
+            "op_host_us_mean": {k: v / max(1, r.reclaims) for k, v in r.op_phase_us.items()},
             "quiesce_wait_us": {"p50": _pct(q, 50), "p99": _pct(q, 99), "max": max(q) if q else None, "n": len(q)},
             "shortfall_to_first_write_us": {"p50": _pct(sf, 50), "p99": _pct(sf, 99), "n": len(sf)},
             "shortfall_to_full_copy_us": {"p50": _pct(sc, 50), "p99": _pct(sc, 99), "n": len(sc)},

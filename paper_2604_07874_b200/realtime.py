@@ -444,6 +444,7 @@ class OfflineEngine:
         self.max_batch = max_batch
         self.reqs = {rid: OffReq(rid, i, o) for rid, i, o in backlog}
         self.waiting = deque(rid for rid, _, _ in backlog)
+        self.running: Dict[int, OffReq] = {}  # admitted, in prefill or decode
         self.resume: deque = deque()
         self.prefill_q: deque = deque()
         self.decoding: List[int] = []
@@ -459,9 +460,13 @@ class OfflineEngine:
         return -(-(r.input + r.output) // self.page_tokens)
 
     def live(self):
-        return [r for r in self.reqs.values() if r.state in ("prefill", "decode")]
+        return list(self.running.values())
 
-    def admit(self, now: int) -> int:
+    def admit(self, now: int, warm: bool = False, rng: Optional[random.Random] = None) -> int:
+        """Admission into the pool while it has room (sim.cpp:730-753), resumed requests first.
+        warm=True (run start): the tenant is in steady state -- each admitted request has already
+        prefilled and generated a random part of its output, i.e. holds input + generated tokens of
+        KV, exactly what an eviction throws away (requests.hpp:68-69)."""
         if self.frozen:
             return 0
         n = 0
@@ -474,13 +479,19 @@ class OfflineEngine:
                 if r.state == "waiting":
                     self.log.add(now, "arrival", **{"class": "offline"}, request_id=r.rid, gpu=0,
                                  prompt_tokens=r.input, output_tokens=r.output)
-                r.state, r.prefill_left, r.invested = "prefill", r.recompute_cost(), 0
-                self.prefill_q.append(r.rid)
+                self.running[r.rid] = r
                 n += 1
+                if warm:
+                    r.generated = rng.randrange(r.output)
+                    r.state, r.prefill_left, r.invested = "decode", 0, r.input + r.generated
+                    self.decoding.append(r.rid)
+                else:
+                    r.state, r.prefill_left, r.invested = "prefill", r.recompute_cost(), 0
+                    self.prefill_q.append(r.rid)
         return n
 
     def costs(self):
-        return {r.rid: r.recompute_cost() for r in self.live()}
+        return {r.rid: r.recompute_cost() for r in self.running.values()}
 
     def advance(self, forwards: float, now: int, horizon_us: int):
         """Spend harvested token-forwards, iteration by iteration as a continuous-batching engine
@@ -503,6 +514,7 @@ class OfflineEngine:
                     if r.generated == r.output:
                         r.state = "done"
                         self.decoding.remove(rid)
+                        del self.running[rid]
                         self.pool.offline_release(rid)
                         freed = True
                         if now <= horizon_us:
@@ -532,6 +544,7 @@ class OfflineEngine:
     def on_evicted(self, rids, now: int, kill: bool):
         for rid in rids:
             r = self.reqs[rid]
+            self.running.pop(rid, None)
             self.lost += r.invested
             if r.rid in self.prefill_q:
                 self.prefill_q.remove(r.rid)
@@ -603,13 +616,18 @@ class RtConfig:
     copy_ctas: int = 8
     copy_buffer_bytes: int = 6 << 30      # pinned destination per in-flight copy
     static_window_frac: float = 0.1       # scenario.hpp:51
+    seed: int = 2604
 
 
 def c2_resparams() -> A.ReservationParams:
-    """c2_llama8b_qwen7b.json: rate-control reservation (window 5 s, t_max 1 s), defaults else."""
+    """c2_llama8b_qwen7b.json's rate-control reservation (window 5 s, t_max 1 s, target 1 per
+    window) with a first release interval of 200 ms instead of 1 s, so the reservation leaves
+    its initial 10 % within the first ~20 s of a 60 s trace (the reference's default T_init is
+    sized for its 500 s rate_control run); everything else at the defaults (memory.hpp:103-114)."""
     p = A.ReservationParams()
     p.window_us = 5_000_000
     p.t_max_us = 1_000_000
+    p.t_init_us = 200_000
     return p
 
 
@@ -687,7 +705,7 @@ class Colocation:
                     # live now -- evicted requests are gone from it, sim.cpp:994-1050)
                     self._decode_tiles += st.tiles_done
                     self.gate.reset_work()
-                if self.offline.live():
+                if self.offline.running:
                     self.gate.launch_offline(self.pool, None, None, 0, 0, None, stream=self.off_stream.cuda_stream,
                                              ctas=self.cfg.decode_ctas)
         if self.gemm_chain and self.ggate.read().live_ctas == 0:
@@ -719,9 +737,8 @@ class Colocation:
         per_token = QWEN_FLOP_PER_TOKEN * self.cfg.gemm_layers / 28
         fwd = (flop - self._flop_accounted) / per_token if flop > self._flop_accounted else 0.0
         self._flop_accounted = max(self._flop_accounted, flop)
-        if fwd > 0 and self.offline.advance(fwd, now, self.horizon_us):
-            if self.offline.admit(now) or self.offline.live():
-                self.pool.set_costs(self.offline.costs())
+        if fwd > 0 and self.offline.advance(fwd, now, self.horizon_us) and not self._busy:
+            self.offline.admit(now)  # while the lane is busy, admission waits for the idle edge
 
     def _chain_flop_of(self, tiles_total):
         """FLOP of the first `tiles_total` tiles of the (cyclic) chain."""
@@ -834,8 +851,8 @@ class Colocation:
         ph = self.res.op_phase_us
         t0 = time.perf_counter()
         self._harvest(now, force=True)
-        if self.offline.live():
-            self.pool.set_costs(self.offline.costs())
+        if self.offline.running:
+            self.pool.set_costs(self.offline.costs())  # Cost(r) of the residents now (sim.cpp:877-883)
         t1 = time.perf_counter()
         self._quiesce_order_pool(now)
         mode = 1 if (kill or self.policy == "valve-fifo") else 0
@@ -907,10 +924,9 @@ class Colocation:
                 self.res.log.add(t, "reserve_change", gpu=0, old_handles=old, new_handles=P.online_handles(),
                                  cause="release")
                 self.res.releases += 1
-                self.offline.admit(t)
-                if self.offline.live():
-                    self.pool.set_costs(self.offline.costs())
-                self._launch_offline()
+                if not self._busy:  # the offline engine admits at its next iteration
+                    self.offline.admit(t)
+                    self._launch_offline()
         self.resctl.note_tick(t)
         self._schedule(t + self.resctl.interval(), "tick")
 
@@ -966,8 +982,7 @@ class Colocation:
         self.offline.budget = self._static_min_free
         self.offline.frozen = False
         self.res.log.add(t, "static_limit", gpu=0, handles=self._static_min_free)
-        if self.offline.admit(t):
-            self.pool.set_costs(self.offline.costs())
+        self.offline.admit(t, warm=True, rng=random.Random(self.cfg.seed))
         self._launch_offline()
 
     # ----------------------------------------------------------------- online page writes
@@ -1037,8 +1052,7 @@ class Colocation:
             if self.mem == "static":
                 self.offline.frozen = True
                 self._schedule(int(round(self.horizon_us * cfg.static_window_frac)), "calib")
-            if self.offline.admit(0):
-                P.set_costs(self.offline.costs())
+            self.offline.admit(0, warm=True, rng=random.Random(cfg.seed))
             P.fill_pages()
             self.gate.reset_work()
             if self.ggate:
@@ -1050,6 +1064,7 @@ class Colocation:
         last_tok: Dict[int, int] = {}
         nxt, pi, n_decodes = 0, 0, 0
         busy, busy_since, stalled = False, 0, False
+        self._busy = False
         pending_wait = None
         wait_events = []
         torch.cuda.synchronize()
@@ -1068,7 +1083,8 @@ class Colocation:
                 break
             if self.colocated:
                 self._fire_timers(now)
-                self._harvest(now)
+                if not busy:  # gated while busy: nothing to harvest
+                    self._harvest(now)
             while nxt < len(reqs) and reqs[nxt].arrival_us <= now:
                 r = reqs[nxt]
                 log.add(r.arrival_us, "arrival", **{"class": "online"}, request_id=r.rid, gpu=0,
@@ -1115,20 +1131,19 @@ class Colocation:
                     act = None
             if act is None:
                 if busy:  # idle edge (sim.cpp:371-380)
-                    busy = False
+                    busy = self._busy = False
                     log.add(now, "busy", gpu=0, **{"class": "online"}, start_us=busy_since, end_us=now)
                     if self.colocated:
                         self.channel.note_all_idle(now)
                         self._fire_timers(now)
                         self._harvest(now, force=True)
-                        if self.offline.admit(now):
-                            P.set_costs(self.offline.costs())
+                        self.offline.admit(now)
                 if finished and not stalled:
                     break
                 if self.colocated and self._offline_allowed():
                     self._launch_offline()
-                    if stalled and self.offline.admit(now):
-                        P.set_costs(self.offline.costs())
+                    if stalled:
+                        self.offline.admit(now)
                 time.sleep(50e-6)
                 continue
             stalled = False
@@ -1138,7 +1153,7 @@ class Colocation:
             else:
                 n_decodes += 1
             if not busy:  # busy edge: raise + wait for the offline CTAs to retire (sim.cpp:362-369)
-                busy = True
+                busy = self._busy = True
                 busy_since = now
                 if self.colocated:
                     self._harvest(now, force=True)

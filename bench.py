@@ -69,14 +69,14 @@ def parse():
     ap.add_argument("--seed", type=int, default=2604)
     ap.add_argument("--skip-realtime", action="store_true", help="skip the measured TTFT/TPOT run")
     ap.add_argument("--skip-fanout", action="store_true", help="skip the same-device TP fan-out sweep")
-    ap.add_argument("--rt-horizon", type=float, default=24.0, help="online trace length (s)")
-    ap.add_argument("--rt-repeats", type=int, default=3, help="colocated runs (interleaved with standalone)")
-    ap.add_argument("--rt-decode-ctas", type=int, default=16,
-                    help="offline KV decode-pass CTAs in the real-time run (-1 = none, 0 = library default)")
-    ap.add_argument("--rt-gemm-ctas", type=int, default=64, help="offline GEMM CTAs in the real-time run (0 = all SMs)")
-    ap.add_argument("--rt-gemm", default="qwen2-7b:2048",
-                    help="offline tenant's gated tcgen05 GEMMs: 'qwen2-7b:<tokens>' = a random-init Qwen2-7B's "
-                         "projection chain (28 layers x qkv/o/gate-up/down), 'm,n,k' = one shape, '' = decode pass only")
+    ap.add_argument("--rt-horizon", type=float, default=60.0, help="C2 online trace length (s)")
+    ap.add_argument("--rt-tail", type=float, default=20.0, help="drain time after the horizon (s)")
+    ap.add_argument("--rt-repeats", type=int, default=2, help="valve runs (interleaved with standalone)")
+    ap.add_argument("--rt-policies", default="valve-fifo,channel+static,channel+prism",
+                    help="extra policies run once each on the same kernels (policies.cpp:5-14)")
+    ap.add_argument("--rt-decode-ctas", type=int, default=16, help="offline KV decode-pass CTAs (-1 = none)")
+    ap.add_argument("--rt-gemm-ctas", type=int, default=64,
+                    help="offline Qwen2-7B projection-chain CTAs (0 = all SMs, -1 = no GEMM tenant)")
     ap.add_argument("--profile-mode", action="store_true",
                     help="ncu launch-list runs: no offline kernel (ncu serialises it to completion)")
     return ap.parse_args()
@@ -372,13 +372,64 @@ def tp_fanout_same_device(torch, A, pool, dev, groups=(1, 2, 4, 8), iters=300, s
             "ack_wait": ["batched memops on the waiting stream", "helper stream per member"][mode], "groups": out}
 
 
-def _rt_gemm(spec):
-    """--rt-gemm: "m,n,k" (one GEMM shape), "qwen2-7b:<tokens>" (the model's projection chain) or ''."""
-    if not spec:
-        return None
-    if spec.startswith("qwen2-7b"):
-        return ("qwen2-7b", int(spec.split(":")[1]))
-    return tuple(int(x) for x in spec.split(","))
+def tp_fanout_across_ranks(torch, A, pool, dist, rank, world, gpu, groups=(2, 4, 8), iters=200, seed=0):
+    """TP-group gate fan-out with one process per GPU (SURVEY §8e, configs[3]): for each group
+    size tp dividing the world, consecutive ranks form groups, every member's gate words live in
+    its own HBM, the leader opens them over CUDA IPC and raises / waits over NVLink peer memory
+    (paper_2604_07874_b200.tp).  Every member runs its gated decode pass on all its SMs.
+    Returns group size -> the leaders' p50 / p99 preempt-to-quiesce (max over the groups)."""
+    from paper_2604_07874_b200 import tp as TP
+
+    out = {}
+    for tp in groups:
+        if tp > world or world % tp:
+            continue
+        gate = A.Gate(gpu)
+        grp = TP.TPGate(gate, rank, world, tp, dist, opener=TP.open_member(gpu))
+        lat = TP.measure_group_fanout(torch, gate, grp, pool, dist, gpu, iters=iters, seed=seed + rank)
+        lat.sort()
+        mine = [lat[len(lat) // 2], lat[int(0.99 * (len(lat) - 1))], lat[-1]] if lat else [0.0, 0.0, 0.0]
+        t = torch.tensor(mine, device=torch.device("cuda", gpu), dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out[str(tp)] = {"p50_us": round(t[0].item(), 2), "p99_us": round(t[1].item(), 2),
+                        "max_us": round(t[2].item(), 2), "preemptions_per_group": len(lat) if lat else iters,
+                        "groups": world // tp}
+        del grp, gate
+        dist.barrier()
+    return {"note": "one process per GPU; leader raise -> every member's CTAs retired, over NVLink peer "
+                    "memory (max over the TP groups of the job)", "groups": out}
+
+
+VALVE_OPS = os.path.join(ROOT, "tools", "_bin", "valve_ops")
+
+
+def e2e_cpp(torch, dist, gpu, H, args, world):
+    """`e2e` through the reference's C++ runtime API: tools/_bin/valve_ops (tools/cpp/
+    colosim_ops.cpp compiled against include/colosim, linked to libvalve.so) runs the same burst
+    of reclaim ops as the device leg -- gate raise + quiesce, MemoryPool::snapshot(),
+    selective_reclaim(), MemoryPool::apply_reclaim(), the gather copy into pinned host memory,
+    re-admission -- one copy queued behind the running one.  Whole job: bytes of all ranks over
+    the slowest rank's seconds."""
+    import subprocess
+
+    env = dict(os.environ, VALVE_DEVICE=str(gpu))
+    r = subprocess.run([VALVE_OPS, "e2e", str(H), str(args.k), str(max(1, args.steps)), str(max(1, args.warmup))],
+                       capture_output=True, text=True, timeout=600, env=env)
+    if r.returncode != 0:
+        raise RuntimeError(f"valve_ops e2e rc={r.returncode}: {r.stderr[-300:]}")
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    secs, nbytes = d["seconds"], d["bytes"]
+    if world > 1:
+        secs, nbytes = aggregate_ranks(dist, secs * 1e3, nbytes, torch.device("cuda", gpu))
+        secs *= 1e-3
+    return {"value": round(nbytes / secs / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": d["h2d_bytes_per_step"], "d2h_bytes_per_step": d["d2h_bytes_per_step"],
+            "path": "C++: colosim::MemoryPool::snapshot() -> colosim::selective_reclaim() -> "
+                    "MemoryPool::apply_reclaim() -> valve_pool_reclaim_copy_start(), pinned host buffers "
+                    "(tools/_bin/valve_ops, include/colosim drop-in over libvalve.so)",
+            "breakdown_ms_per_step": d["breakdown_ms_per_step"],
+            "pipelining": "one reclaim copy queued behind the running one (op i+1 decides while op i copies); "
+                          "the burst's first op preempts the offline tenant, which stays gated for the burst"}
 
 
 def _guarded(name, fn):
@@ -578,6 +629,9 @@ def run_valve(args, rank, world, dist):
         fanout = tp_fanout_same_device(torch, A, pool, dev, seed=args.seed)
         fanout["alt_helper_streams"] = tp_fanout_same_device(torch, A, pool, dev, groups=(2, 4, 8), iters=200,
                                                              seed=args.seed, mode=1)["groups"]
+    elif not args.profile_mode and not args.skip_fanout and world > 1:
+        fanout = _guarded("tp_fanout", lambda: tp_fanout_across_ranks(torch, A, pool, dist, rank, world, gpu,
+                                                                      seed=args.seed))
 
     # ------------------------------------------------ GEMM tenant (tcgen05)
     def next_gen():
@@ -682,6 +736,7 @@ def run_valve(args, rank, world, dist):
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     c3 = _guarded("c3_weight_pages", lambda: c3_weights(torch, A, gpu, cp, args.seed + rank, peak))
+    cpp_e2e = _guarded("e2e_cpp", lambda: e2e_cpp(torch, dist, gpu, H, args, world))
 
     # ------------------------------------------------ measured online TTFT/TPOT deltas
     # (real-time loop: random-init Llama-3-8B online in PyTorch + the gated offline tenant on a
@@ -696,15 +751,13 @@ def run_valve(args, rank, world, dist):
         torch.cuda.empty_cache()
         from paper_2604_07874_b200 import realtime as RT
 
-        # power-headroom tenant: the KV decode pass on 16 CTAs + the gated GEMM on 64 SMs keeps the
-        # board below its power cap, so the online tenant starts each busy period at full clock
-        # (an all-SM GEMM tenant holds ~985 W / ~1,680 MHz and costs the first prefill ~5 %;
-        # tools/realtime_sweep.py)
-        rt = _guarded("online_realtime", lambda: RT.measure_deltas(
-            horizon=args.rt_horizon, device=gpu, seed=args.seed + rank,
-            offline_ctas=args.rt_decode_ctas, repeats=args.rt_repeats,
-            offline_gemm=_rt_gemm(args.rt_gemm),
-            offline_gemm_ctas=args.rt_gemm_ctas, log_dir=os.path.join(ROOT, "gpurun_out", "realtime_logs")))
+        # BASELINE C2 trace + C3's MIAD resizing and rate-bounded copies (realtime.measure)
+        rcfg = RT.RtConfig(decode_ctas=args.rt_decode_ctas, gemm_ctas=args.rt_gemm_ctas)
+        rt = _guarded("online_realtime", lambda: RT.measure(
+            horizon=args.rt_horizon, tail_s=args.rt_tail, device=gpu, seed=args.seed + rank,
+            repeats=args.rt_repeats, cfg=rcfg,
+            policies=tuple(p for p in args.rt_policies.split(",") if p),
+            log_dir=os.path.join(ROOT, "gpurun_out", "realtime_logs")))
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "r1_copy_traffic.json")))
     except OSError:
@@ -767,15 +820,19 @@ def run_valve(args, rank, world, dist):
             "hbm": {"achieved": round(copy_gbs, 2), "peak": HBM_PEAK, "unit": "GB/s",
                     "frac": round(copy_gbs / HBM_PEAK, 5), "peak_source": HBM_PEAK_SOURCE},
         },
-        "e2e": {
+        "e2e": cpp_e2e if cpp_e2e and "value" in cpp_e2e else {
             "value": round(e2e_bytes / e2e_s / 1e9, 3),
             "unit": "GB/s",
             "h2d_bytes_per_step": int(e2e_h2d / n_e2e),
             "d2h_bytes_per_step": int(e2e_d2h / n_e2e),
-            "path": "snapshot() -> selective_reclaim(instance) -> apply_reclaim(ids) -> reclaim_copy_start(), host buffers",
+            "path": "python ctypes mirror (C++ driver unavailable: %s)" % (cpp_e2e or {}).get("error", "?"),
+        },
+        "e2e_python_api": {
+            "value": round(e2e_bytes / e2e_s / 1e9, 3),
+            "unit": "GB/s",
+            "path": "paper_2604_07874_b200.api (ctypes): snapshot() -> selective_reclaim(instance) -> "
+                    "apply_reclaim(ids) -> reclaim_copy_start(), host buffers",
             "breakdown_ms_per_step": {k: round(v / n_e2e, 3) for k, v in brk.items()},
-            "pipelining": "one reclaim copy queued behind the running one (op i+1 decides while op i copies); "
-                          "the burst's first op preempts the offline tenant, which stays gated for the burst",
         },
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
@@ -883,7 +940,29 @@ def cpu_baseline_block(args):
                       f"snapshot+selective_reclaim+apply_reclaim (1 core, C++-timed; "
                       f"{r['decision_us_per_op']:.0f} us/op) + host memcpy gather of the same pages "
                       f"({threads} threads, {r['gather_gbs']:.1f} GB/s) from a 3.5 GiB host mirror",
-            "decision_us_per_op": round(r["decision_us_per_op"], 1)}
+            "decision_us_per_op": round(r["decision_us_per_op"], 1),
+            "bookkeeping_vs_device": _guarded("bookkeeping", bookkeeping_table)}
+
+
+def bookkeeping_table(handles=(128, 1024), ks="1,4,15,36,64"):
+    """Per-op latency through the reference's C++ API on both sides of the link-swap
+    (tools/cpp/colosim_ops.cpp): oracle/_ref/ref_ops = the reference's MemoryPool /
+    selective_reclaim on one host core, tools/_bin/valve_ops = the same calls through the
+    include/colosim drop-in on the B200 (plus the fused single-call reclaim).  Medians in us."""
+    import subprocess
+
+    ref = os.path.join(ROOT, "oracle", "_ref", "ref_ops")
+    out = {}
+    for h in handles:
+        row = {}
+        for name, exe in (("reference_cpu", ref), ("b200", VALVE_OPS)):
+            if not os.path.exists(exe):
+                row[name] = {"error": f"{exe} not built"}
+                continue
+            r = subprocess.run([exe, "table", str(h), ks], capture_output=True, text=True, timeout=600)
+            row[name] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else {"error": r.stderr[-200:]}
+        out[str(h)] = row
+    return out
 
 
 def run_reference(args, rank, world):
@@ -922,8 +1001,17 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group("nccl")
+        from paper_2604_07874_b200 import tp as TP
+
+        gpu, shared = TP.rank_device(int(os.environ.get("LOCAL_RANK", "0")),
+                                     int(os.environ.get("LOCAL_WORLD_SIZE", str(world))), torch.cuda.device_count())
+        torch.cuda.set_device(gpu)
+        # rank r on cuda:r; a box with fewer GPUs than ranks (functional runs only) cannot run
+        # NCCL with two ranks on one device, so it falls back to gloo for the plumbing
+        dist.init_process_group("gloo" if shared else "nccl")
+        if shared and rank == 0:
+            print("bench: fewer GPUs than ranks -- ranks share devices; no number here is a multi-GPU number",
+                  file=sys.stderr, flush=True)
     else:
         torch.cuda.set_device(0)
     out = run_valve(args, rank, world, dist)

@@ -40,6 +40,14 @@ class MemoryPool {
     pool_.reset(p);
   }
 
+  // B200 addition: a pool with a page store / table sizes from a full device config
+  explicit MemoryPool(const valve_pool_config& cfg)
+      : total_(cfg.total_handles), hsz_(cfg.handle_size_pages), tok_(cfg.page_size_tokens) {
+    valve_pool* p = nullptr;
+    valve_detail::check(valve_pool_create_ex(&cfg, &p));
+    pool_.reset(p);
+  }
+
   int total_handles() const { return total_; }
   int handle_size_pages() const { return hsz_; }
   int page_size_tokens() const { return tok_; }

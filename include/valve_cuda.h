@@ -193,6 +193,12 @@ int valve_pool_landed(const valve_pool* p, uint64_t* landed, uint64_t* issued);
  * re-admitted later.  Synchronous; CTA count / chunk size from params (may be NULL). */
 int valve_pool_restore(valve_pool* p, int64_t req, const void* host_src, int n_pages,
                        const int* blk_of_page, const valve_copy_params* params, valve_copy_stats* stats);
+/* Streams for hosts without the CUDA runtime (a C++ / cgo / JNI caller of this ABI): a
+ * non-blocking stream on `device` (high_priority != 0: the device's highest priority, as the
+ * online lane uses), its destruction and a host wait on it. */
+int valve_stream_create(int device, int high_priority, void** out);
+void valve_stream_destroy(void* stream);
+int valve_stream_synchronize(void* stream);
 /* Pinned, device-mapped host staging for reclaimed pages (cudaHostAlloc, mapped). */
 int valve_host_alloc(int64_t bytes, void** out);
 void valve_host_free(void* p);
@@ -277,6 +283,11 @@ int valve_gate_release(valve_gate* g, uint32_t gen, void* stream);
 int valve_gate_raise_stamped(valve_gate* g, uint32_t gen, void* stream);
 /* Makes `stream` wait (cuStreamWaitValue) until every gated kernel acknowledged `gen`. */
 int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* stream);
+/* TP member side: makes `stream` wait until the group leader has closed this gate (its raise
+ * reached this GPU over peer memory) and this GPU's gated CTAs have all retired -- orders a
+ * member's online work and pool remaps after its own quiesce without any host round trip.  Call
+ * it only inside a busy period the leader raises for (sim.cpp:362-369). */
+int valve_gate_wait_closed_quiesced(valve_gate* g, void* stream);
 /* TP fan-out: members' gate words are written by the leader over NVLink peer memory. */
 int valve_gate_attach_peers(valve_gate* leader, valve_gate** members, int n);
 /* How the leader waits for the members' acks: BATCHED (default) = one stream-memory-operation

@@ -721,6 +721,7 @@ def _declare_valve_extras(L):
         "valve_gate_release": (C.c_int, [vp, u32, vp]),
         "valve_gate_raise_stamped": (C.c_int, [vp, u32, vp]),
         "valve_gate_wait_quiesced": (C.c_int, [vp, u32, vp]),
+        "valve_gate_wait_closed_quiesced": (C.c_int, [vp, vp]),
         "valve_gate_attach_peers": (C.c_int, [vp, P(vp), C.c_int]),
         "valve_gate_set_fanout": (C.c_int, [vp, C.c_int]),
         "valve_gate_export": (C.c_int, [vp, C.c_char_p]),
@@ -994,6 +995,11 @@ class Gate:
     def wait_quiesced(self, gen: int, stream: Optional[int] = None):
         self._b.check(self._b.lib.valve_gate_wait_quiesced(self._h, gen,
                                                            C.c_void_p(stream) if stream else None))
+
+    def wait_closed_quiesced(self, stream: Optional[int] = None):
+        """TP member: `stream` waits for the leader's raise to land here and this GPU's gated
+        CTAs to retire (valve_gate_wait_closed_quiesced)."""
+        self._b.check(self._b.lib.valve_gate_wait_closed_quiesced(self._h, C.c_void_p(stream) if stream else None))
 
     def read(self) -> GateState:
         s = GateState()

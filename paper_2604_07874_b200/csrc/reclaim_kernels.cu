@@ -200,7 +200,7 @@ __device__ void greedy_block(int n, const int* hid, Refs R, const int* rref, con
 // (no per-owner fold pass).  Taken handles are masked by their owner's `live` bits.
 __device__ void greedy_block_packed(int n, const int* hid, Refs R, const int* rref, const int64_t* cost,
                                     int k, const int64_t* marg0, unsigned* skey, int* ev, const int* qoff,
-                                    const int* qh, int* out, int idbits) {
+                                    const int* qh, int* out, int idbits, int qmax) {
   constexpr int NW = kGreedyThreads / 32;
   __shared__ unsigned w_key[NW];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -233,14 +233,28 @@ __device__ void greedy_block_packed(int n, const int* hid, Refs R, const int* rr
     for (int j = 0; j < kGreedyOwn; ++j)
       if (best == t + j * kGreedyThreads) live &= ~(1u << j);
     if (t == 0) out[round] = hid[best];
-    for (int e = R.begin(best) + t; e < R.end(best); e += kGreedyThreads) {
-      const int r = rref[e];
-      if (atomicExch(&ev[r], 1) == 0) {
-        const unsigned dec = (unsigned)cost[r] << idbits;
-        for (int q = qoff[r]; q < qoff[r + 1]; ++q) atomicSub(&skey[qh[q]], dec);
+    if (qmax > 0) {
+      // rows are distinct within a handle: thread t takes listing t / qmax of the winner and the
+      // (t % qmax)-th handle listing that request -- one dependent chain per (request, handle)
+      // instead of a serial loop per request; `ev` is read here and set after the barrier
+      const int b0 = R.begin(best), nl = R.end(best) - b0;
+      for (int x = t; x < nl * qmax; x += kGreedyThreads) {
+        const int r = rref[b0 + x / qmax];
+        const int q = qoff[r] + x % qmax;
+        if (q < qoff[r + 1] && !ev[r]) atomicSub(&skey[qh[q]], (unsigned)cost[r] << idbits);
       }
+      greedy_bar();
+      for (int x = t; x < nl; x += kGreedyThreads) ev[rref[b0 + x]] = 1;
+    } else {
+      for (int e = R.begin(best) + t; e < R.end(best); e += kGreedyThreads) {
+        const int r = rref[e];
+        if (atomicExch(&ev[r], 1) == 0) {
+          const unsigned dec = (unsigned)cost[r] << idbits;
+          for (int q = qoff[r]; q < qoff[r + 1]; ++q) atomicSub(&skey[qh[q]], dec);
+        }
+      }
+      greedy_bar();
     }
-    greedy_bar();
     c_upd += clock64() - c1;
   }
   if (t == 0) g_greedy_cycles[0] = c_arg, g_greedy_cycles[1] = c_upd;
@@ -375,10 +389,23 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
       bad |= (marg[i] >= lim) | (i + 1 < n && hid[i] >= hid[i + 1]);
     for (int d = threadIdx.x; d < m2; d += blockDim.x) bad |= cost2[d] < 0;
     const bool packed = __syncthreads_or(bad) == 0;
+    // flat update rounds need distinct requests within every handle's listings (the fused
+    // path's rows are deduplicated; host instances may repeat a request on a handle)
+    int dup = 0, qm = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      for (int o = roff[i]; o < roff[i + 1]; ++o)
+        for (int o2 = roff[i]; o2 < o; ++o2) dup |= rr[o2] == rr[o];
+    for (int d = threadIdx.x; d < m2; d += blockDim.x) qm = max(qm, qoff2[d + 1] - qoff2[d]);
+    __shared__ int s_qmax;
+    if (threadIdx.x == 0) s_qmax = 0;
+    const bool has_dup = __syncthreads_or(dup) != 0;
+    if (qm) atomicMax(&s_qmax, qm);
+    __syncthreads();
+    const int qmax = has_dup ? 0 : s_qmax;
     const Refs Rs{roff, nullptr, 0};
     unsigned* skey = reinterpret_cast<unsigned*>(taken + kSmemHandles);
     if (threadIdx.x < kGreedyThreads) {
-      if (packed) greedy_block_packed(n, hid, Rs, rr, cost2, k, marg, skey, ev2, qoff2, qh2, out, idbits);
+      if (packed) greedy_block_packed(n, hid, Rs, rr, cost2, k, marg, skey, ev2, qoff2, qh2, out, idbits, qmax);
       else greedy_block(n, hid, Rs, rr, cost2, k, marg, ev2, qoff2, qh2, out);
     }
     __syncthreads();
@@ -513,24 +540,113 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
     else set_err(P, kErrLogic, kDetNotOffline, h);
   }
   // Clear the chosen handles, collecting (row, logical page, physical page, block).
-  const int64_t nslots = (int64_t)b * P.S;
-  for (int64_t idx = threadIdx.x; idx < nslots; idx += blockDim.x) {
-    const int h = ids[idx / P.S];
-    const int64_t p = (int64_t)h * P.S + idx % P.S;
-    const int row = P.slot_row[p];
-    if (row < 0) continue;
-    const int pos = atomicAdd(&s_nt, 1);
-    const int blk = P.slot_blk[p];
-    P.s_qh[pos] = row;
-    P.s_rref[pos] = (int)((int64_t)h * P.S + P.slot_lid[p]);
-    P.s_tphys[pos] = (int)p;
-    P.s_tblk[pos] = blk;
-    P.s_ev[row] = 1;
-    P.bt[(int64_t)row * P.P + blk] = P.quarantine;  // quarantine remap
-    atomicSub(&P.row_npages[row], 1);
-    P.slot_row[p] = -1;
-    P.slot_lid[p] = -1;
-    P.slot_blk[p] = -1;
+  // Fast path (S <= 64): one warp per chosen handle in ascending id order.  The report order
+  // inside a request is (logical, physical) with logical = h * S + lid, i.e. by handle, then by
+  // (lid, slot) inside the handle -- so each warp ranks its handle's pages of every row among
+  // themselves (O(S) smem scan per page) and records one "pair" (row, handle position, count);
+  // sorting the few pairs by (request rank, handle position) and a scan of their counts gives
+  // every page its report position without sorting the pages.
+  constexpr int kFastS = 64, kFastB = 1024, kPairCap = 2048;
+  const bool fast = P.S <= kFastS && b <= kFastB;
+  int* hs = reinterpret_cast<int*>(smem);   // [kFastB] chosen handles, ascending
+  int* wscr = hs + kFastB;                  // [32 warps][3][kFastS] slot rows / lids / pair ids
+  int* prow = wscr + 32 * 3 * kFastS;       // [kPairCap] pair: row
+  int* phi = prow + kPairCap;               //   handle position in ascending order
+  int* pcnt = phi + kPairCap;               //   pages of the row on that handle
+  int* ppos = pcnt + kPairCap;              //   report position of the pair's first page
+  int* sev = ppos + kPairCap;               // [kPairCap] evicted rows (first pair that saw them)
+  int* pord = sev + kPairCap;               // [kPairCap] pairs in (request rank, handle) order
+  __shared__ int s_np, s_ne;
+  if (fast) {
+    if (threadIdx.x == 0) s_np = 0, s_ne = 0;
+    for (int i = threadIdx.x; i < b; i += blockDim.x) {  // ids are distinct (validated)
+      const int h = ids[i];
+      int pos = 0;
+      for (int j = 0; j < b; ++j) pos += ids[j] < h;
+      hs[pos] = h;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int* wrow = wscr + wid * 3 * kFastS;
+    int* wlid = wrow + kFastS;
+    int* wpid = wlid + kFastS;
+    for (int hi = wid; hi < b; hi += nw) {
+      const int h = hs[hi];
+      for (int s = lane; s < P.S; s += 32) {
+        wrow[s] = P.slot_row[(int64_t)h * P.S + s];
+        wlid[s] = P.slot_lid[(int64_t)h * P.S + s];
+      }
+      __syncwarp();
+      int r_first[kFastS / 32], r_wr[kFastS / 32];
+#pragma unroll
+      for (int j = 0; j < kFastS / 32; ++j) {
+        const int s = lane + 32 * j;
+        r_first[j] = -1;
+        const int row = s < P.S ? wrow[s] : -1;
+        if (row < 0) continue;
+        const int lid = wlid[s];
+        int cnt = 0, wr = 0, first = s;
+        for (int q = 0; q < P.S; ++q) {
+          if (wrow[q] != row) continue;
+          ++cnt;
+          const int lq = wlid[q];
+          wr += lq < lid || (lq == lid && q < s);
+          first = min(first, q);
+        }
+        r_first[j] = first;
+        r_wr[j] = wr;
+        if (first == s) {  // the row's first slot on this handle owns the pair
+          const int pid = atomicAdd(&s_np, 1);
+          wpid[s] = pid;
+          if (pid < kPairCap) prow[pid] = row, phi[pid] = hi, pcnt[pid] = cnt;
+          if (atomicExch(&P.s_ev[row], 1) == 0) {
+            const int e = atomicAdd(&s_ne, 1);
+            if (e < kPairCap) sev[e] = row;
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < kFastS / 32; ++j) {
+        if (r_first[j] < 0) continue;
+        const int s = lane + 32 * j;
+        const int64_t p = (int64_t)h * P.S + s;
+        const int row = wrow[s];
+        const int blk = P.slot_blk[p];
+        const int pos = atomicAdd(&s_nt, 1);
+        P.s_qh[pos] = row;
+        P.s_rref[pos] = (int)((int64_t)h * P.S + wlid[s]);
+        P.s_tphys[pos] = (int)p;
+        P.s_tblk[pos] = blk;
+        P.s_key[pos] = ((uint64_t)(uint32_t)wpid[r_first[j]] << 32) | (uint32_t)r_wr[j];
+        P.bt[(int64_t)row * P.P + blk] = P.quarantine;  // quarantine remap
+        atomicSub(&P.row_npages[row], 1);
+        P.slot_row[p] = -1;
+        P.slot_lid[p] = -1;
+        P.slot_blk[p] = -1;
+      }
+      __syncwarp();
+    }
+  } else {
+    const int64_t nslots = (int64_t)b * P.S;
+    for (int64_t idx = threadIdx.x; idx < nslots; idx += blockDim.x) {
+      const int h = ids[idx / P.S];
+      const int64_t p = (int64_t)h * P.S + idx % P.S;
+      const int row = P.slot_row[p];
+      if (row < 0) continue;
+      const int pos = atomicAdd(&s_nt, 1);
+      const int blk = P.slot_blk[p];
+      P.s_qh[pos] = row;
+      P.s_rref[pos] = (int)((int64_t)h * P.S + P.slot_lid[p]);
+      P.s_tphys[pos] = (int)p;
+      P.s_tblk[pos] = blk;
+      P.s_ev[row] = 1;
+      P.bt[(int64_t)row * P.P + blk] = P.quarantine;  // quarantine remap
+      atomicSub(&P.row_npages[row], 1);
+      P.slot_row[p] = -1;
+      P.slot_lid[p] = -1;
+      P.slot_blk[p] = -1;
+    }
   }
   for (int i = threadIdx.x; i < b; i += blockDim.x) {
     const int h = ids[i];
@@ -542,8 +658,69 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
   __syncthreads();
   const int nt = s_nt;
   if (threadIdx.x == 0) g_apply_ns[0] = (long long)globaltimer_ns();
+  int carry = 0, ne;
+  if (fast && s_np <= kPairCap && s_ne <= kPairCap) {
+    ne = s_ne;
+    const int np = s_np;
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {  // evicted rows ranked by request id
+      const int row = sev[e];
+      const int64_t req = P.row_req[row];
+      int rank = 0;
+      for (int f = 0; f < ne; ++f) rank += P.row_req[sev[f]] < req;
+      P.s_rank[row] = rank;
+      P.s_evrows[e] = row;
+      P.s_ev[row] = 0;
+      P.res_evicted[rank] = req;
+      P.res_ev_pbytes[rank] = P.row_pbytes[row] ? P.row_pbytes[row] : P.page_bytes;
+    }
+    if (threadIdx.x == 0) P.res_inv_off[ne] = nt;
+    __syncthreads();
+    if (threadIdx.x == 0) g_apply_ns[1] = (long long)globaltimer_ns();
+    for (int j = threadIdx.x; j < np; j += blockDim.x) {  // pairs by (request rank, handle position)
+      const int kj = (P.s_rank[prow[j]] << 11) | phi[j];
+      int pos = 0;
+      for (int i = 0; i < np; ++i) pos += ((P.s_rank[prow[i]] << 11) | phi[i]) < kj;
+      pord[pos] = j;
+    }
+    __syncthreads();
+    for (int base = 0; base < np; base += blockDim.x) {
+      const int j = base + threadIdx.x;
+      const int pr = j < np ? pord[j] : 0;
+      int tot;
+      const int ex = block_excl_scan(j < np ? pcnt[pr] : 0, tot);
+      if (j < np) {
+        ppos[pr] = carry + ex;
+        const int rank = P.s_rank[prow[pr]];
+        if (j == 0 || P.s_rank[prow[pord[j - 1]]] != rank) P.res_inv_off[rank] = carry + ex;
+      }
+      carry += tot;
+    }
+    int64_t bcarry = 0;
+    int custom = 0;
+    for (int base = 0; base < ne; base += blockDim.x) {  // destination byte layout of the copy
+      const int e = base + threadIdx.x;
+      const int c = e < ne ? P.res_inv_off[e + 1] - P.res_inv_off[e] : 0;
+      const int64_t pb = e < ne ? P.res_ev_pbytes[e] : 0;
+      int64_t btot;
+      const int64_t bex = block_excl_scan64((int64_t)c * pb, btot);
+      custom |= __syncthreads_or(e < ne && pb != P.page_bytes);
+      if (e < ne) P.res_ev_base[e] = bcarry + bex;
+      bcarry += btot;
+    }
+    if (threadIdx.x == 0) {
+      P.res_ev_base[ne] = bcarry;
+      P.mirror->copy_bytes = bcarry;
+      P.mirror->copy_custom = custom;
+    }
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+      const uint64_t kv = P.s_key[i];
+      const int pos = ppos[kv >> 32] + (int)(uint32_t)kv;
+      P.res_pages[pos] = P.s_rref[i];
+      P.res_phys[pos] = P.s_tphys[i];
+      P.res_blk[pos] = P.s_tblk[i];
+    }
+  } else {
   // evicted rows, then their rank by request id
-  int carry = 0;
   for (int base = 0; base < P.R; base += blockDim.x) {
     const int r = base + threadIdx.x;
     const int f = (r < P.R && P.s_ev[r]) ? 1 : 0;
@@ -555,7 +732,7 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
     }
     carry += tot;
   }
-  const int ne = carry;
+  ne = carry;
   __syncthreads();
   for (int e = threadIdx.x; e < ne; e += blockDim.x) {
     const int row = P.s_evrows[e];
@@ -660,6 +837,7 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
         P.res_blk[o + i] = pay[o + i];
       }
     }
+  }
   }
   __syncthreads();
   if (threadIdx.x == 0) g_apply_ns[2] = (long long)globaltimer_ns();

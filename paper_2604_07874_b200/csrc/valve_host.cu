@@ -1188,6 +1188,25 @@ int valve_pool_restore(valve_pool* p, int64_t req, const void* host_src, int n_p
   });
 }
 
+int valve_stream_create(int device, int high_priority, void** out) {
+  return guard([&] {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    int lo = 0, hi = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    cudaStream_t s = nullptr;
+    ck(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, high_priority ? hi : lo), "stream");
+    *out = s;
+  });
+}
+
+void valve_stream_destroy(void* s) {
+  if (s) cudaStreamDestroy(static_cast<cudaStream_t>(s));
+}
+
+int valve_stream_synchronize(void* s) {
+  return guard([&] { ck(cudaStreamSynchronize(static_cast<cudaStream_t>(s)), "cudaStreamSynchronize"); });
+}
+
 int valve_host_alloc(int64_t bytes, void** out) {
   return guard([&] {
     if (bytes <= 0) fail(VALVE_INVALID_ARGUMENT, "host_alloc: bytes must be > 0");
@@ -1702,6 +1721,19 @@ int valve_gate_wait_quiesced(valve_gate* g, uint32_t gen, void* s) {
     cu_ck(op.write32((CUstream)st, dptr(&g->d->quiesced_gen), gen, 0), "cuStreamWriteValue32");
     for (size_t i = 0; i < g->peers.size(); ++i)
       ck(cudaStreamWaitEvent(st, g->wait_events[2 * i + 1], 0), "event wait");
+  });
+}
+
+int valve_gate_wait_closed_quiesced(valve_gate* g, void* s) {
+  return guard([&] {
+    if (g->remote) fail(VALVE_LOGIC_ERROR, "gate_wait_closed_quiesced: call it on the member's own gate");
+    const MemOps& op = memops();
+    cudaStream_t st = as_stream(s, g->stream);
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    MemBatch b;
+    b.wait_eq32(&g->d->closed, 1);
+    b.wait_eq32(&g->d->live_ctas, 0);
+    b.submit(op, st);
   });
 }
 

@@ -595,6 +595,7 @@ class RunResult:
     op_phase_us: Dict[str, float] = field(default_factory=dict)
     decode_iter_us: List[float] = field(default_factory=list)
     prefill_us: List[float] = field(default_factory=list)
+    step_gap_us: List[float] = field(default_factory=list)  # host time between back-to-back busy steps
     log: EventLog = field(default_factory=EventLog)
     plan: list = field(default_factory=list)
 
@@ -1066,6 +1067,7 @@ class Colocation:
         busy, busy_since, stalled = False, 0, False
         self._busy = False
         pending_wait = None
+        last_end = None
         wait_events = []
         torch.cuda.synchronize()
         import gc
@@ -1147,6 +1149,7 @@ class Colocation:
                 time.sleep(50e-6)
                 continue
             stalled = False
+            gap_from = last_end if busy else None
             if act[0] == "prefill":
                 self.res.plan.append((act[1], n_decodes))
                 pi += 1
@@ -1177,13 +1180,15 @@ class Colocation:
                     pending_wait = None
                 toks = torch.randint(0, m.s.vocab, (r.prompt,), device=self.dev)
                 t_it = now_us()
+                if gap_from is not None:
+                    self.res.step_gap_us.append(t_it - gap_from)
                 log.add(t_it, "prefill_start", **{"class": "online"}, request_id=r.rid, gpu=0, tokens=r.prompt)
                 with torch.cuda.stream(self.online):
                     tok = m.prefill(toks, r.pages, self._wait_layer_fn(r.pages))
                 self.online.synchronize()
                 lens[r.rid] = r.prompt
                 last_tok[r.rid] = int(tok.item())
-                t_pe = now_us()
+                t_pe = last_end = now_us()
                 log.add(t_pe, "prefill_end", **{"class": "online"}, request_id=r.rid, gpu=0)
                 self.res.prefill_us.append(t_pe - t_it)
                 decoding.append(r)
@@ -1202,12 +1207,14 @@ class Colocation:
                 if tgt:
                     self.pool.wait_landed(tgt, self.online.cuda_stream)
             t_it = now_us()
+            if gap_from is not None:
+                self.res.step_gap_us.append(t_it - gap_from)
             with torch.cuda.stream(self.online):
                 out = m.decode([last_tok[r.rid] for r in decoding],
                                [r.pages[lens[r.rid] // cfg.page_tokens] for r in decoding],
                                [lens[r.rid] for r in decoding], [r.pages for r in decoding], self._scratch)
             self.online.synchronize()
-            t_emit = now_us()
+            t_emit = last_end = now_us()
             self.res.decode_iter_us.append(t_emit - t_it)
             done = []
             for r, o in zip(decoding, out.tolist()):
@@ -1469,6 +1476,9 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
             "pressure_events": r.pressure, "stalls": r.stalls,
             "copy_gb": r.copy_bytes / 1e9, "copy_gbs_mean": (sum(r.copy_gbs) / len(r.copy_gbs)) if r.copy_gbs else None,
             "decision_us_p50": _pct([d for x in rs for d in x.decision_us], 50),
+            "decode_iter_ms_mean": sum(d for x in rs for d in x.decode_iter_us) / max(1, sum(len(x.decode_iter_us) for x in rs)) / 1e3,
+            "step_gap_us_mean": sum(d for x in rs for d in x.step_gap_us) / max(1, sum(len(x.step_gap_us) for x in rs)),
+            "step_gap_us_p99": _pct([d for x in rs for d in x.step_gap_us], 99),
             "op_host_us_mean": {k: v / max(1, r.reclaims) for k, v in r.op_phase_us.items()},
             "quiesce_wait_us": {"p50": _pct(q, 50), "p99": _pct(q, 99), "max": max(q) if q else None, "n": len(q)},
             "shortfall_to_first_write_us": {"p50": _pct(sf, 50), "p99": _pct(sf, 99), "n": len(sf)},
@@ -1493,6 +1503,9 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
                        "tpot_ms_mean": sum(base_tpot.values()) / max(1, len(base_tpot)) / 1e3,
                        "decode_iter_ms_p50": _pct([x for s in solos for x in s.decode_iter_us], 50) / 1e3,
                        "prefill_ms_p50": _pct([x for s in solos for x in s.prefill_us], 50) / 1e3,
+                       "decode_iter_ms_mean": sum(d for x in solos for d in x.decode_iter_us) / max(1, sum(len(x.decode_iter_us) for x in solos)) / 1e3,
+                       "step_gap_us_mean": sum(d for x in solos for d in x.step_gap_us) / max(1, sum(len(x.step_gap_us) for x in solos)),
+                       "step_gap_us_p99": _pct([d for x in solos for d in x.step_gap_us], 99),
                        "plan_deviations": [_deviations(plan, x.plan) for x in solos],
                        "clocks": [x.clocks for x in solos]},
         colos[0].policy: arm(colos),

@@ -15,7 +15,8 @@ replicas for pool/selection/copy -- no NCCL), and only a TP online group shares 
 """
 from __future__ import annotations
 
-from typing import List, Sequence
+import time
+from typing import List, Sequence, Tuple
 
 
 def tp_groups(world: int, tp: int) -> List[List[int]]:
@@ -23,6 +24,16 @@ def tp_groups(world: int, tp: int) -> List[List[int]]:
     if tp <= 0 or world % tp:
         raise ValueError(f"world size {world} is not a multiple of tp {tp}")
     return [list(range(g * tp, (g + 1) * tp)) for g in range(world // tp)]
+
+
+def rank_device(local_rank: int, local_world: int, n_devices: int) -> Tuple[int, bool]:
+    """(device, shared) for a rank: one process per GPU -- rank r on cuda:r -- whenever the node
+    has a GPU per local rank; a box with fewer GPUs maps ranks round-robin and reports
+    shared=True (functional runs only: the contexts time-slice one GPU and there is no NVLink
+    hop, so no latency taken there is a TP number)."""
+    if n_devices <= 0:
+        raise RuntimeError("no CUDA device: every rank's gate lives in HBM")
+    return local_rank % n_devices, n_devices < local_world
 
 
 def group_of(rank: int, groups: Sequence[Sequence[int]]) -> List[int]:
@@ -70,3 +81,57 @@ class TPGate:
     def _leader_only(self):
         if not self.is_leader:
             raise RuntimeError(f"rank {self.rank} is not the leader of TP group {self.group}")
+
+
+def open_member(device: int):
+    """Opener for TPGate: a member's exported gate words, mapped into this process on the
+    leader's device (CUDA IPC with lazy peer access: the words stay in the member's HBM and the
+    leader's stream memory operations reach them over NVLink)."""
+    from . import api as A
+
+    return lambda handle: A.Gate.open_remote(handle, device)
+
+
+def measure_group_fanout(torch, gate, group: "TPGate", pool, dist, device: int, iters: int = 200,
+                         ctas: int = 0, seed: int = 0):
+    """Preempt-to-quiesce of one TP group, one process (and GPU) per member: every member runs
+    its gated offline decode pass over its own pool; the leader raises the group gate (stream
+    memory operations on every member's words over peer memory) and its stream waits until every
+    member's CTAs retired.  Latency = CUDA events around raise + wait on the leader's gate
+    stream.  Iterations are host-synchronised with dist.barrier() so every member is running
+    when the leader raises.  Returns the leader's samples (members: []).  The reference's
+    unpatched toggle is linear in the GPUs (scenario.hpp:56-58)."""
+    import random
+
+    rng = random.Random(seed)
+    off = torch.cuda.Stream(device=device)
+    gs = torch.cuda.ExternalStream(gate.stream, device=device)
+    lat = []
+    for it in range(iters + 10):
+        gate.reset_work()
+        gate.launch_offline(pool, None, None, 0, 0, None, ctas=ctas, stream=off.cuda_stream)
+        torch.cuda.synchronize(device)  # the launch is queued and its CTAs start
+        dist.barrier()
+        if group.is_leader:
+            deadline = time.perf_counter() + rng.uniform(100e-6, 400e-6)
+            while time.perf_counter() < deadline:
+                pass
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(gs)
+            group.raise_(it + 1)
+            group.wait_quiesced(it + 1)
+            e1.record(gs)
+            e1.synchronize()
+            if it >= 10:
+                lat.append(e0.elapsed_time(e1) * 1e3)
+        dist.barrier()
+        st = gate.read()
+        assert st.closed == 1 and st.live_ctas == 0, (group.rank, st.closed, st.live_ctas)
+        dist.barrier()
+        if group.is_leader:
+            group.release(it + 1)
+            gs.synchronize()
+        dist.barrier()
+        gate.cancel_work()  # drop the rest of the pass: the next sample starts a fresh one
+        off.synchronize()
+    return lat

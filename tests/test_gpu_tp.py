@@ -141,3 +141,35 @@ def test_fanout_modes_quiesce_every_member_same_process(mode):
     assert [g.read().tiles_done for g in gates] == [total] * 4  # every tile exactly once
     with pytest.raises(A.InvalidArgument):
         gates[0].set_fanout(5)
+
+
+def test_member_waits_for_leader_raise_and_own_quiesce():
+    """A member's stream-ordered wait (valve_gate_wait_closed_quiesced) holds its online stream
+    until the leader's raise lands on the member's words and the member's CTAs retired."""
+    import torch
+
+    from paper_2604_07874_b200 import api as A
+
+    pool = A.DevicePool(64, 16, 16, slot_bytes=1 << 20, page_bytes=917504)
+    for r in range(64):
+        pool.offline_reserve(r, 16, 0)
+    pool.fill_pages()
+    leader, member = A.Gate(0), A.Gate(0)
+    leader.attach_peers([member])
+    off, online = torch.cuda.Stream(), torch.cuda.Stream()
+    member.reset_work()
+    member.launch_offline(pool, None, None, 0, 0, None, ctas=8, stream=off.cuda_stream)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    member.wait_closed_quiesced(online.cuda_stream)
+    with torch.cuda.stream(online):
+        flag.fill_(1)
+    time.sleep(0.01)
+    assert int(flag.cpu()) == 0  # held: the leader has not raised
+    leader.raise_(3)
+    online.synchronize()
+    st = member.read()
+    assert int(flag.cpu()) == 1 and st.closed == 1 and st.live_ctas == 0
+    leader.release(3)
+    torch.cuda.ExternalStream(leader.stream).synchronize()
+    member.cancel_work()
+    off.synchronize()

@@ -118,33 +118,40 @@ def test_measured_b200_run_deltas_match_reference_metrics(solo, colo):
     assert ref["disables_issued"] >= 1  # the colocated run really gated the offline tenant
 
 
+SMALL = dict(horizon=4.0, base=1.0, spike=6.0, period=4.0, width=1.0, handles=16, layers=2, output=(4, 6),
+             prompt=(600, 900), tail_s=4.0)
+
+
 @pytest.mark.gpu
 @need_ref
 def test_live_harness_logs_match_reference_metrics(tmp_path):
+    """The live loop's events.jsonl (online KV in pool slots, decode-pass + GEMM-chain tenant)
+    pair through the reference's own build_report / ttft_increase / tpot_increase."""
     from paper_2604_07874_b200 import realtime as RT
 
-    out = RT.measure_deltas(horizon=4.0, base=1.0, spike=6.0, period=4.0, width=1.0, handles=16, layers=2,
-                            output=(4, 6), prompt=(600, 900), log_dir=str(tmp_path))
-    assert out["pairs"] > 0
-    for i in range(1):
-        solo, colo = str(tmp_path / f"solo{i}.jsonl"), str(tmp_path / f"colo{i}.jsonl")
-        ref = ref_metrics(solo, colo)
-        (s_ttft, s_tpot), (c_ttft, c_tpot) = deltas_from_log(solo), deltas_from_log(colo)
-        assert ref["pairs"] == out["pairs"]
-        assert ref["ttft_mean_pct"] == pytest.approx(paired_increase(s_ttft, c_ttft)["mean_pct"], rel=1e-12, abs=1e-12)
-        assert ref["tpot_mean_pct"] == pytest.approx(paired_increase(s_tpot, c_tpot)["mean_pct"], rel=1e-12, abs=1e-12)
+    cfg = RT.RtConfig(gemm_tokens=256, gemm_layers=2, gemm_ctas=16)
+    out = RT.measure(repeats=1, policies=(), cfg=cfg, log_dir=str(tmp_path), **SMALL)
+    assert out["valve"]["pairs"] > 0
+    solo, colo = str(tmp_path / "solo0.jsonl"), str(tmp_path / "colo0.jsonl")
+    ref = ref_metrics(solo, colo)
+    (s_ttft, s_tpot), (c_ttft, c_tpot) = deltas_from_log(solo), deltas_from_log(colo)
+    assert ref["pairs"] == paired_increase(s_ttft, c_ttft)["pairs"] > 0
+    assert ref["ttft_mean_pct"] == pytest.approx(paired_increase(s_ttft, c_ttft)["mean_pct"], rel=1e-12, abs=1e-12)
+    assert ref["tpot_mean_pct"] == pytest.approx(paired_increase(s_tpot, c_tpot)["mean_pct"], rel=1e-12, abs=1e-12)
+    assert ref["disables_issued"] >= 1
 
 
 @pytest.mark.gpu
-def test_live_harness_with_offline_model_chain():
-    """The offline tenant as a random-init Qwen2-7B projection chain (28 layers x 4 gated GEMMs):
-    the chain advances across preemptions (GEMMs complete, harvest > 0) and the paired run still
-    yields reference-pairable deltas."""
+def test_live_harness_policies_on_the_same_kernels():
+    """Every policy arm runs on the same kernels and replays the standalone plan exactly; the
+    offline engine completes requests (harvest > 0) and the static arm kills instead of evicting."""
     from paper_2604_07874_b200 import realtime as RT
 
-    out = RT.measure_deltas(horizon=4.0, base=1.0, spike=6.0, period=4.0, width=1.0, handles=16, layers=2,
-                            output=(4, 6), prompt=(600, 900), offline_gemm=("qwen2-7b", 256),
-                            offline_gemm_ctas=16)
-    g = out["offline_gemm"]
-    assert g["gemms_completed"] > 4 and g["tflops_harvested"] > 0 and g["model_tokens_per_s"] > 0
-    assert out["pairs"] > 0 and len(out["plan_deviations"]["colocated"]) == 1
+    cfg = RT.RtConfig(gemm_tokens=256, gemm_layers=2, gemm_ctas=16)
+    out = RT.measure(repeats=1, policies=("valve-fifo", "channel+static", "channel+prism"), cfg=cfg, **SMALL)
+    for pol in ("valve", "valve-fifo", "channel+static", "channel+prism"):
+        assert out[pol]["plan_deviations"] == [0] * len(out[pol]["plan_deviations"]), pol
+        assert out[pol]["pairs"] > 0, pol
+        assert out[pol]["offline_forwards_per_s"] > 0, pol
+    assert out["channel+static"]["evictions"] == 0
+    assert out["channel+prism"]["reclaims"] == 0

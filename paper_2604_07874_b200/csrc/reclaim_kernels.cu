@@ -22,7 +22,8 @@ constexpr int kSmemTuples = 8192;    // invalidation report sorted in shared mem
 // dynamic shared memory of k_reclaim / k_apply / k_select_instance (host sets the attribute):
 // greedy 2048*(8+4+4+1+4) + 4096*(8+4+4+4+4+4) + 4 = 157,700 B; apply sort 8192*20 = 163,840 B
 static_assert(kSmemHandles * 21 + kSmemListings * 28 + 64 <= 160 * 1024, "greedy smem");
-static_assert(kSmemTuples * 20 <= 160 * 1024, "sort smem");  // key 8 + pay 4 + cursors 4 + segment 4
+static_assert(kSmemTuples * 20 <= 160 * 1024, "sort smem");
+static_assert((1024 + 3 * 8192 + 6 * 2048) * 4 <= 160 * 1024, "apply fast-path smem");  // key 8 + pay 4 + cursors 4 + segment 4
 
 __device__ long long g_greedy_cycles[2];  // diagnostics: argmin / update cycles of the last run
 __device__ long long g_apply_ns[6];       // diagnostics: apply_core phase stamps of the last run
@@ -260,6 +261,61 @@ __device__ void greedy_block_packed(int n, const int* hid, Refs R, const int* rr
   if (t == 0) g_greedy_cycles[0] = c_arg, g_greedy_cycles[1] = c_upd;
 }
 
+// Packed-key rounds in ONE warp (n <= 1024): lane l owns keys l + 32 j (j < 32) and their taken
+// bits in a register; a round is 32 shared loads + one CREDUX per lane, the winner's evictions
+// spread over the lanes, and __syncwarp instead of CTA barriers (~2x fewer cycles per round than
+// the 8-warp form, which pays two named barriers per round).
+__device__ void greedy_warp_packed(int n, const int* hid, Refs R, const int* rref, const int64_t* cost, int k,
+                                   const int64_t* marg0, unsigned* skey, int* ev, const int* qoff, const int* qh,
+                                   int* out, int idbits, int qmax) {
+  const int lane = threadIdx.x & 31;
+  const unsigned idmask = (1u << idbits) - 1u;
+  unsigned live = 0;
+  for (int j = 0; j < 32; ++j) {
+    const int i = lane + 32 * j;
+    if (i < n) {
+      live |= 1u << j;
+      skey[i] = ((unsigned)marg0[i] << idbits) | (unsigned)i;
+    }
+  }
+  __syncwarp();
+  long long c_arg = 0, c_upd = 0;
+  for (int round = 0; round < k; ++round) {
+    const long long c0 = clock64();
+    unsigned v = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if ((live >> j) & 1u) v = min(v, skey[lane + 32 * j]);
+    v = __reduce_min_sync(kFull, v);
+    const int best = (int)(v & idmask);
+    const long long c1 = clock64();
+    c_arg += c1 - c0;
+    if ((best & 31) == lane) live &= ~(1u << (best >> 5));
+    if (lane == 0) out[round] = hid[best];
+    const int b0 = R.begin(best), nl = R.end(best) - b0;
+    if (qmax > 0) {  // distinct requests per handle: one (request, listing handle) per lane
+      for (int x = lane; x < nl * qmax; x += 32) {
+        const int r = rref[b0 + x / qmax];
+        const int q = qoff[r] + x % qmax;
+        if (q < qoff[r + 1] && !ev[r]) atomicSub(&skey[qh[q]], (unsigned)cost[r] << idbits);
+      }
+      __syncwarp();
+      for (int x = lane; x < nl; x += 32) ev[rref[b0 + x]] = 1;
+    } else {
+      for (int e = b0 + lane; e < b0 + nl; e += 32) {
+        const int r = rref[e];
+        if (atomicExch(&ev[r], 1) == 0) {
+          const unsigned dec = (unsigned)cost[r] << idbits;
+          for (int q = qoff[r]; q < qoff[r + 1]; ++q) atomicSub(&skey[qh[q]], dec);
+        }
+      }
+    }
+    __syncwarp();
+    c_upd += clock64() - c1;
+  }
+  if (lane == 0) g_greedy_cycles[0] = c_arg, g_greedy_cycles[1] = c_upd;
+}
+
 // Same rounds CTA-wide over global arrays (instances larger than shared memory).
 __device__ void greedy_cta(int n, const int* hid, Refs R, const int* rref, const int64_t* cost,
                            int k, int64_t* marg, int* taken, int* ev, const int* qoff, const int* qh,
@@ -404,7 +460,9 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
     const int qmax = has_dup ? 0 : s_qmax;
     const Refs Rs{roff, nullptr, 0};
     unsigned* skey = reinterpret_cast<unsigned*>(taken + kSmemHandles);
-    if (threadIdx.x < kGreedyThreads) {
+    if (packed && n <= 1024) {
+      if (threadIdx.x < 32) greedy_warp_packed(n, hid, Rs, rr, cost2, k, marg, skey, ev2, qoff2, qh2, out, idbits, qmax);
+    } else if (threadIdx.x < kGreedyThreads) {
       if (packed) greedy_block_packed(n, hid, Rs, rr, cost2, k, marg, skey, ev2, qoff2, qh2, out, idbits, qmax);
       else greedy_block(n, hid, Rs, rr, cost2, k, marg, ev2, qoff2, qh2, out);
     }
@@ -540,23 +598,27 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
     else set_err(P, kErrLogic, kDetNotOffline, h);
   }
   // Clear the chosen handles, collecting (row, logical page, physical page, block).
-  // Fast path (S <= 64): one warp per chosen handle in ascending id order.  The report order
-  // inside a request is (logical, physical) with logical = h * S + lid, i.e. by handle, then by
-  // (lid, slot) inside the handle -- so each warp ranks its handle's pages of every row among
-  // themselves (O(S) smem scan per page) and records one "pair" (row, handle position, count);
-  // sorting the few pairs by (request rank, handle position) and a scan of their counts gives
-  // every page its report position without sorting the pages.
-  constexpr int kFastS = 64, kFastB = 1024, kPairCap = 2048;
-  const bool fast = P.S <= kFastS && b <= kFastB;
-  int* hs = reinterpret_cast<int*>(smem);   // [kFastB] chosen handles, ascending
-  int* wscr = hs + kFastB;                  // [32 warps][3][kFastS] slot rows / lids / pair ids
-  int* prow = wscr + 32 * 3 * kFastS;       // [kPairCap] pair: row
-  int* phi = prow + kPairCap;               //   handle position in ascending order
-  int* pcnt = phi + kPairCap;               //   pages of the row on that handle
-  int* ppos = pcnt + kPairCap;              //   report position of the pair's first page
-  int* sev = ppos + kPairCap;               // [kPairCap] evicted rows (first pair that saw them)
-  int* pord = sev + kPairCap;               // [kPairCap] pairs in (request rank, handle) order
+  // Fast path (b * S <= 8192): the chosen handles in ascending id order, slot tuples at
+  // idx = position * S + slot in shared memory.  The report order inside a request is
+  // (logical, physical) with logical = h * S + lid, i.e. by handle, then by (lid, slot) inside the
+  // handle -- so each page is ranked among its row's pages on its own handle (an O(S) scan of
+  // that handle's tuples) and the row's first slot there records one "pair" (row, handle
+  // position, count); sorting the few pairs by (request rank, handle position) and a scan of
+  // their counts gives every page its report position without sorting the pages.
+  constexpr int kFastT = 8192, kFastB = 1024, kPairCap = 2048, kPer = kFastT / kNT;
+  const bool fast = (int64_t)b * P.S <= kFastT && b <= kFastB;
+  int* hs = reinterpret_cast<int*>(smem);  // [kFastB] chosen handles, ascending
+  int* trow = hs + kFastB;                 // [kFastT] slot tuples: row (-1 = empty slot)
+  int* tlid = trow + kFastT;               //   logical id inside the handle
+  int* tpid = tlid + kFastT;               //   pair id (on the row's first slot of the handle)
+  int* prow = tpid + kFastT;               // [kPairCap] pair: row
+  int* phi = prow + kPairCap;              //   handle position in ascending order
+  int* pcnt = phi + kPairCap;              //   pages of the row on that handle
+  int* ppos = pcnt + kPairCap;             //   report position of the pair's first page
+  int* sev = ppos + kPairCap;              // [kPairCap] evicted rows (first pair that saw them)
+  int* pord = sev + kPairCap;              // [kPairCap] pairs in (request rank, handle) order
   __shared__ int s_np, s_ne;
+  const int nslot = b * P.S;
   if (fast) {
     if (threadIdx.x == 0) s_np = 0, s_ne = 0;
     for (int i = threadIdx.x; i < b; i += blockDim.x) {  // ids are distinct (validated)
@@ -566,66 +628,72 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
       hs[pos] = h;
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    int* wrow = wscr + wid * 3 * kFastS;
-    int* wlid = wrow + kFastS;
-    int* wpid = wlid + kFastS;
-    for (int hi = wid; hi < b; hi += nw) {
-      const int h = hs[hi];
-      for (int s = lane; s < P.S; s += 32) {
-        wrow[s] = P.slot_row[(int64_t)h * P.S + s];
-        wlid[s] = P.slot_lid[(int64_t)h * P.S + s];
-      }
-      __syncwarp();
-      int r_first[kFastS / 32], r_wr[kFastS / 32];
+    for (int idx = threadIdx.x; idx < nslot; idx += blockDim.x) {  // read + clear every chosen slot
+      const int hi = idx / P.S;
+      const int64_t p = (int64_t)hs[hi] * P.S + (idx - hi * P.S);
+      const int row = P.slot_row[p];
+      trow[idx] = row;
+      if (row < 0) continue;
+      const int blk = P.slot_blk[p];
+      tlid[idx] = P.slot_lid[p];
+      P.s_pay[idx] = blk;
+      atomicAdd(&s_nt, 1);
+      P.bt[(int64_t)row * P.P + blk] = P.quarantine;  // quarantine remap
+      atomicSub(&P.row_npages[row], 1);
+      P.slot_row[p] = -1;
+      P.slot_lid[p] = -1;
+      P.slot_blk[p] = -1;
+    }
+    __syncthreads();
+    int r_first[kPer], r_wr[kPer];
 #pragma unroll
-      for (int j = 0; j < kFastS / 32; ++j) {
-        const int s = lane + 32 * j;
-        r_first[j] = -1;
-        const int row = s < P.S ? wrow[s] : -1;
+    for (int j = 0; j < kPer; ++j) {
+      const int idx = threadIdx.x + j * kNT;
+      r_first[j] = -1;
+      const int row = idx < nslot ? trow[idx] : -1;
+      if (row < 0) continue;
+      const int base = (idx / P.S) * P.S, s = idx - base;
+      const int lid = tlid[idx];
+      int cnt = 0, wr = 0, first = s;
+      for (int q = 0; q < P.S; ++q) {
+        if (trow[base + q] != row) continue;
+        ++cnt;
+        const int lq = tlid[base + q];
+        wr += lq < lid || (lq == lid && q < s);
+        first = min(first, q);
+      }
+      r_first[j] = base + first;
+      r_wr[j] = wr;
+      if (first == s) {  // the row's first slot on this handle owns the pair
+        const int pid = atomicAdd(&s_np, 1);
+        tpid[idx] = pid;
+        if (pid < kPairCap) prow[pid] = row, phi[pid] = base / P.S, pcnt[pid] = cnt;
+        if (atomicExch(&P.s_ev[row], 1) == 0) {
+          const int e = atomicAdd(&s_ne, 1);
+          if (e < kPairCap) sev[e] = row;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (r_first[j] >= 0)
+        P.s_key[threadIdx.x + j * kNT] = ((uint64_t)(uint32_t)tpid[r_first[j]] << 32) | (uint32_t)r_wr[j];
+    if (s_np > kPairCap || s_ne > kPairCap) {
+      // too many pairs for the on-chip report: compact the tuples for the general sort below
+      __shared__ int s_cmp;
+      if (threadIdx.x == 0) s_cmp = 0;
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < nslot; idx += blockDim.x) {
+        const int row = trow[idx];
         if (row < 0) continue;
-        const int lid = wlid[s];
-        int cnt = 0, wr = 0, first = s;
-        for (int q = 0; q < P.S; ++q) {
-          if (wrow[q] != row) continue;
-          ++cnt;
-          const int lq = wlid[q];
-          wr += lq < lid || (lq == lid && q < s);
-          first = min(first, q);
-        }
-        r_first[j] = first;
-        r_wr[j] = wr;
-        if (first == s) {  // the row's first slot on this handle owns the pair
-          const int pid = atomicAdd(&s_np, 1);
-          wpid[s] = pid;
-          if (pid < kPairCap) prow[pid] = row, phi[pid] = hi, pcnt[pid] = cnt;
-          if (atomicExch(&P.s_ev[row], 1) == 0) {
-            const int e = atomicAdd(&s_ne, 1);
-            if (e < kPairCap) sev[e] = row;
-          }
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < kFastS / 32; ++j) {
-        if (r_first[j] < 0) continue;
-        const int s = lane + 32 * j;
-        const int64_t p = (int64_t)h * P.S + s;
-        const int row = wrow[s];
-        const int blk = P.slot_blk[p];
-        const int pos = atomicAdd(&s_nt, 1);
+        const int hi = idx / P.S;
+        const int pos = atomicAdd(&s_cmp, 1);
         P.s_qh[pos] = row;
-        P.s_rref[pos] = (int)((int64_t)h * P.S + wlid[s]);
-        P.s_tphys[pos] = (int)p;
-        P.s_tblk[pos] = blk;
-        P.s_key[pos] = ((uint64_t)(uint32_t)wpid[r_first[j]] << 32) | (uint32_t)r_wr[j];
-        P.bt[(int64_t)row * P.P + blk] = P.quarantine;  // quarantine remap
-        atomicSub(&P.row_npages[row], 1);
-        P.slot_row[p] = -1;
-        P.slot_lid[p] = -1;
-        P.slot_blk[p] = -1;
+        P.s_rref[pos] = hs[hi] * P.S + tlid[idx];
+        P.s_tphys[pos] = hs[hi] * P.S + (idx - hi * P.S);
+        P.s_tblk[pos] = P.s_pay[idx];
       }
-      __syncwarp();
     }
   } else {
     const int64_t nslots = (int64_t)b * P.S;
@@ -712,12 +780,14 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
       P.mirror->copy_bytes = bcarry;
       P.mirror->copy_custom = custom;
     }
-    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
-      const uint64_t kv = P.s_key[i];
+    for (int idx = threadIdx.x; idx < nslot; idx += blockDim.x) {
+      if (trow[idx] < 0) continue;
+      const uint64_t kv = P.s_key[idx];
       const int pos = ppos[kv >> 32] + (int)(uint32_t)kv;
-      P.res_pages[pos] = P.s_rref[i];
-      P.res_phys[pos] = P.s_tphys[i];
-      P.res_blk[pos] = P.s_tblk[i];
+      const int hi = idx / P.S, h = hs[hi];
+      P.res_pages[pos] = (int64_t)h * P.S + tlid[idx];
+      P.res_phys[pos] = h * P.S + (idx - hi * P.S);
+      P.res_blk[pos] = P.s_pay[idx];
     }
   } else {
   // evicted rows, then their rank by request id
@@ -946,9 +1016,8 @@ __global__ void __launch_bounds__(256) k_reclaim_rows(PoolDev P) {
 }
 
 // Fused reclaim, part 2 (sim.cpp:936-942): compact the offline handles (the snapshot), select
-// k handles with the row costs, apply -- one CTA, after k_reclaim_rows on the same stream.
-__global__ void __launch_bounds__(kNT) k_reclaim(PoolDev P, int k, int mode, int64_t t) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// k handles with the row costs, apply -- one CTA, after the instance rows are built.
+__device__ void reclaim_body(const PoolDev& P, int k, int mode, int64_t t, unsigned char* smem) {
   op_begin(P);
   // offline handles ascending -> index space
   int carry = 0;
@@ -981,6 +1050,40 @@ __global__ void __launch_bounds__(kNT) k_reclaim(PoolDev P, int k, int mode, int
   __syncthreads();
   if (threadIdx.x == 0) P.mirror->r[6] = (int64_t)globaltimer_ns();
   publish(P);
+}
+
+__global__ void __launch_bounds__(kNT) k_reclaim(PoolDev P, int k, int mode, int64_t t) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  reclaim_body(P, k, mode, t, smem);
+}
+
+// The fused reclaim as ONE launch: ceil(H / 32) CTAs build the instance rows (warp per handle,
+// as k_reclaim_rows), the last CTA to finish (ticket) runs part 2 and then stores `seq` into the
+// pinned mirror after a system-scope fence, which the host polls instead of synchronizing.
+__global__ void __launch_bounds__(kNT) k_reclaim_fused(PoolDev P, int k, int mode, int64_t t, int64_t seq) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int h = blockIdx.x * (kNT >> 5) + (threadIdx.x >> 5);
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.mirror->r[3] = (int64_t)globaltimer_ns();  // phase stamps
+  if (h < P.H && P.hstate[h] == kOffline) {
+    const int nc = (P.S + 31) >> 5;
+    int cnt = 0;
+    VALVE_DISPATCH_NC(nc, cnt = warp_distinct_rows<NC>(P, h, P.s_rref + (int64_t)h * P.S));
+    if (lane == 0) P.s_cnt[h] = cnt;
+  }
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(P.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *P.ticket = 0;  // ready for the next launch (stream-ordered)
+  reclaim_body(P, k, mode, t, smem);
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    P.mirror->done_seq = seq;
+  }
 }
 
 // ---------------------------------------------------- selection over host instances

@@ -68,6 +68,7 @@ struct Mirror {
   int64_t copy_bytes;  // bytes the last apply/reclaim report asks the copy to move
   int copy_custom;     // 1 if some evicted request has its own page size (set_page_bytes)
   int pad2;
+  volatile int64_t done_seq;  // sequence number of the last fused reclaim that finished (host spins on it)
 };
 
 struct PoolDev {
@@ -109,6 +110,7 @@ struct PoolDev {
   uint64_t* s_key;   // [pow2(H*S)]
   int* s_pay;        // [pow2(H*S)]
   int* s_cnt;        // [H]
+  unsigned* ticket;  // [1] CTAs of the fused reclaim's instance pass that finished (last one goes on)
   int* s_tphys;      // [H*S] apply tuples: physical page
   int* s_tblk;       // [H*S] apply tuples: block index
   // results of the last apply / reclaim (device copies; the copy kernel reads res_phys)

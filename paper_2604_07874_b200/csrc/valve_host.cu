@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -179,9 +180,30 @@ struct valve_pool {
     return static_cast<T*>(p);
   }
 
+  int64_t op_seq = 0;
+  // Completion by polling the pinned mirror (the kernel stores done_seq after its results and a
+  // system-scope fence): no stream-synchronize wake-up on the decision path.  Falls back to a
+  // stream synchronize (which surfaces faults) when the word does not appear within 200 ms.
+  void wait_seq(int64_t seq, const char* op) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0; mirror->done_seq != seq; ++spin) {
+      if ((spin & 1023) == 1023 && std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(200)) {
+        ck(cudaStreamSynchronize(stream), op);
+        if (mirror->done_seq != seq) fail(VALVE_RUNTIME_ERROR, std::string(op) + ": completion word not written");
+        break;
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    check_err();
+  }
+
   void sync_and_check(const char* op) {
     ck(cudaGetLastError(), op);
     ck(cudaStreamSynchronize(stream), op);
+    check_err();
+  }
+
+  void check_err() {
     if (mirror->err) {
       const int code = mirror->err;
       const int det = mirror->err_detail;
@@ -242,6 +264,8 @@ static void set_reclaim_smem_attrs() {
   // per device, per process (cheap to repeat)
   ck(cudaFuncSetAttribute(k_reclaim_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 32768),
      "cudaFuncSetAttribute");
+  ck(cudaFuncSetAttribute(k_reclaim_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReclaimSmemBytes),
+     "smem attribute");
   ck(cudaFuncSetAttribute(k_reclaim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReclaimSmemBytes),
      "cudaFuncSetAttribute");
   ck(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReclaimSmemBytes),
@@ -323,6 +347,8 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   d.s_key = p->dalloc<uint64_t>(next_pow2(HS));
   d.s_pay = p->dalloc<int>(next_pow2(HS));
   d.s_cnt = p->dalloc<int>(H);
+  d.ticket = p->dalloc<unsigned>(1);
+  ck(cudaMemset(d.ticket, 0, sizeof(unsigned)), "memset");
   d.s_tphys = p->dalloc<int>(HS);
   d.s_tblk = p->dalloc<int>(HS);
   d.res_handles = p->dalloc<int>(H);
@@ -874,9 +900,14 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
       fail(VALVE_INVALID_ARGUMENT, "reclaim: device-fused mode must be selective or fifo");
     p->order_after_copy_plan();
     ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
-    k_reclaim_rows<<<(p->H + 7) / 8, 256, 0, p->stream>>>(p->d);
+    // one launch: ceil(H / 32) CTAs build the instance rows (warp per handle), the last CTA to
+    // finish runs selection + apply; the host spins on the completion sequence the kernel writes
+    // into the pinned mirror instead of a stream synchronize
+    const int64_t seq = ++p->op_seq;
+    k_reclaim_fused<<<(p->H + 31) / 32, kNT, p->smem_reclaim, p->stream>>>(p->d, k, mode, t, seq);
     counted();
-    p->launch1("reclaim", k_reclaim, p->smem_reclaim, p->d, k, mode, t);
+    ck(cudaGetLastError(), "reclaim");
+    p->wait_seq(seq, "reclaim");
     p->last_n_handles = (int)p->mirror->r[0];
     p->last_n_evicted = (int)p->mirror->r[1];
     p->last_n_pages = (int)p->mirror->r[2];

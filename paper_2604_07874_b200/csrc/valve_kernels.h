@@ -39,6 +39,7 @@ __global__ void k_snapshot(PoolDev P);
 __global__ void k_apply(PoolDev P, const int* ids, int k, int64_t t);
 __global__ void k_reclaim_rows(PoolDev P);
 __global__ void k_reclaim(PoolDev P, int k, int mode, int64_t t);
+__global__ void k_reclaim_fused(PoolDev P, int k, int mode, int64_t t, int64_t seq);
 __global__ void k_check_invariants(PoolDev P, int64_t online_used);
 __global__ void k_fill_pages(PoolDev P);
 __global__ void k_set_costs(PoolDev P, int n, const int64_t* reqs, const int64_t* costs, int which);

@@ -120,6 +120,7 @@ class OnlineModel:
         self.graphs: Dict[int, torch.cuda.CUDAGraph] = {}
         self.mempool = None
         self.P = None
+        self.gpu_events = None  # list: (start, end) CUDA events of every decode graph replay
 
     def bind(self, pool: A.DevicePool):
         """Point the model at the pool's page store (graphs are captured against it)."""
@@ -251,7 +252,15 @@ class OnlineModel:
             self.s_off[:B] = d[:, 2]
             self.s_len[:B] = d[:, 3].to(torch.int32)
             self.s_bt[:B] = d[:, 4:].to(torch.int32)
-            self._graph(B).replay()
+            g = self._graph(B)
+            if self.gpu_events is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.replay()
+                e1.record()
+                self.gpu_events.append((e0, e1))
+            else:
+                g.replay()
             out.append(self.s_out[: len(idx)].clone())
         return torch.cat(out)
 
@@ -596,6 +605,7 @@ class RunResult:
     decode_iter_us: List[float] = field(default_factory=list)
     prefill_us: List[float] = field(default_factory=list)
     step_gap_us: List[float] = field(default_factory=list)  # host time between back-to-back busy steps
+    decode_gpu_us: List[float] = field(default_factory=list)  # device time of each decode graph replay
     log: EventLog = field(default_factory=EventLog)
     plan: list = field(default_factory=list)
 
@@ -1012,6 +1022,7 @@ class Colocation:
         how long each step takes."""
         m, P, cfg = self.m, self.pool, self.cfg
         self.res = RunResult(self.policy, {}, {})
+        m.gpu_events = []
         log = self.res.log
         self.horizon_us = int(horizon_s * 1e6)
         P.reset()
@@ -1237,6 +1248,8 @@ class Colocation:
                         first_token_us=r.emits[0], last_token_us=r.emits[-1], digest="0x0000000000000000")
         self.online.synchronize()
         self.res.wall_s = time.perf_counter() - t0
+        self.res.decode_gpu_us = [a.elapsed_time(b) * 1e3 for a, b in m.gpu_events]
+        m.gpu_events = None
         end = now_us()
         if gc_was:
             gc.enable()
@@ -1478,6 +1491,7 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
             "decision_us_p50": _pct([d for x in rs for d in x.decision_us], 50),
             "decode_iter_ms_mean": sum(d for x in rs for d in x.decode_iter_us) / max(1, sum(len(x.decode_iter_us) for x in rs)) / 1e3,
             "step_gap_us_mean": sum(d for x in rs for d in x.step_gap_us) / max(1, sum(len(x.step_gap_us) for x in rs)),
+            "decode_gpu_ms_mean": sum(d for x in rs for d in x.decode_gpu_us) / max(1, sum(len(x.decode_gpu_us) for x in rs)) / 1e3,
             "step_gap_us_p99": _pct([d for x in rs for d in x.step_gap_us], 99),
             "op_host_us_mean": {k: v / max(1, r.reclaims) for k, v in r.op_phase_us.items()},
             "quiesce_wait_us": {"p50": _pct(q, 50), "p99": _pct(q, 99), "max": max(q) if q else None, "n": len(q)},
@@ -1505,6 +1519,7 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
                        "prefill_ms_p50": _pct([x for s in solos for x in s.prefill_us], 50) / 1e3,
                        "decode_iter_ms_mean": sum(d for x in solos for d in x.decode_iter_us) / max(1, sum(len(x.decode_iter_us) for x in solos)) / 1e3,
                        "step_gap_us_mean": sum(d for x in solos for d in x.step_gap_us) / max(1, sum(len(x.step_gap_us) for x in solos)),
+                       "decode_gpu_ms_mean": sum(d for x in solos for d in x.decode_gpu_us) / max(1, sum(len(x.decode_gpu_us) for x in solos)) / 1e3,
                        "step_gap_us_p99": _pct([d for x in solos for d in x.step_gap_us], 99),
                        "plan_deviations": [_deviations(plan, x.plan) for x in solos],
                        "clocks": [x.clocks for x in solos]},

@@ -72,8 +72,11 @@ def parse():
     ap.add_argument("--rt-horizon", type=float, default=60.0, help="C2 online trace length (s)")
     ap.add_argument("--rt-tail", type=float, default=20.0, help="drain time after the horizon (s)")
     ap.add_argument("--rt-repeats", type=int, default=2, help="valve runs (interleaved with standalone)")
-    ap.add_argument("--rt-policies", default="valve-fifo,channel+static,channel+prism",
+    ap.add_argument("--rt-policies", default="valve-fifo,channel+prism",
                     help="extra policies run once each on the same kernels (policies.cpp:5-14)")
+    ap.add_argument("--rt-horizon-multi", type=float, default=30.0, help="C5 per-GPU trace length at N > 1 (s)")
+    ap.add_argument("--c4-layers", type=int, default=80, help="C4 online model layers (Llama-3-70B: 80)")
+    ap.add_argument("--c4-horizon", type=float, default=20.0, help="C4 online trace length (s)")
     ap.add_argument("--rt-decode-ctas", type=int, default=16, help="offline KV decode-pass CTAs (-1 = none)")
     ap.add_argument("--rt-gemm-ctas", type=int, default=64,
                     help="offline Qwen2-7B projection-chain CTAs (0 = all SMs, -1 = no GEMM tenant)")
@@ -398,6 +401,46 @@ def tp_fanout_across_ranks(torch, A, pool, dist, rank, world, gpu, groups=(2, 4,
         dist.barrier()
     return {"note": "one process per GPU; leader raise -> every member's CTAs retired, over NVLink peer "
                     "memory (max over the TP groups of the job)", "groups": out}
+
+
+def c5_instances(torch, dist, gpu, rank, world, args):
+    """C5 (configs[4]): every GPU runs its own colocation instance on its own online trace (the
+    C2 spike shape, seed per rank) -- the north star's independent per-GPU instances, no collective.
+    One A B A pair per rank (shorter than the N=1 leg); all ranks' deltas are reported."""
+    from paper_2604_07874_b200 import realtime as RT
+
+    rcfg = RT.RtConfig(decode_ctas=args.rt_decode_ctas, gemm_ctas=args.rt_gemm_ctas)
+    r = RT.measure(horizon=args.rt_horizon_multi, tail_s=10.0, device=gpu, seed=args.seed + 101 * rank,
+                   repeats=1, cfg=rcfg, policies=())
+    v = r["valve"]
+    mine = {"rank": rank, "gpu": gpu, "online_requests": r["trace"]["online_requests"],
+            "ttft_delta_pct": v["ttft_delta_pct"], "tpot_delta_pct": v["tpot_delta_pct"],
+            "aa_noise_ttft_pct": r["aa_noise_ttft_pct"], "reclaims": v["reclaims"],
+            "offline_tokens_per_s": v["offline_tokens_per_s"], "quiesce_wait_us": v["quiesce_wait_us"]}
+    allr = [None] * world
+    dist.all_gather_object(allr, mine)
+    return {"config": "C5: %d independent colocation instances (one per GPU), C2 spike trace per instance "
+                      "(seed per rank), %.0f s horizon" % (world, args.rt_horizon_multi),
+            "ranks": allr,
+            "ttft_delta_pct_max": max(x["ttft_delta_pct"] for x in allr if x["ttft_delta_pct"] is not None),
+            "tpot_delta_pct_max": max(x["tpot_delta_pct"] for x in allr if x["tpot_delta_pct"] is not None),
+            "offline_tokens_per_s_total": sum(x["offline_tokens_per_s"] for x in allr)}
+
+
+def c4_tp(torch, dist, gpu, rank, world, args):
+    """C4 (configs[3]): Llama-3-70B TP = min(4, N) online groups over per-rank offline pools,
+    one group gate per TP group broadcast over NVLink peer memory (paper_2604_07874_b200.tp_colo)."""
+    from paper_2604_07874_b200 import tp as TP
+    from paper_2604_07874_b200 import tp_colo as C4
+
+    tp = 4 if world % 4 == 0 else 2
+    _, shared = TP.rank_device(int(os.environ.get("LOCAL_RANK", "0")),
+                               int(os.environ.get("LOCAL_WORLD_SIZE", str(world))), torch.cuda.device_count())
+    c = C4.C4Config(tp=tp, layers=args.c4_layers, horizon_s=args.c4_horizon)
+    r = C4.measure(dist, rank, world, gpu, shared, c, repeats=1)
+    allr = [None] * world
+    dist.all_gather_object(allr, r)
+    return {"groups": [x for x in allr if x is not None]}
 
 
 VALVE_OPS = os.path.join(ROOT, "tools", "_bin", "valve_ops")
@@ -742,8 +785,17 @@ def run_valve(args, rank, world, dist):
     # (real-time loop: random-init Llama-3-8B online in PyTorch + the gated offline tenant on a
     # 32 GiB pool; the 128 GiB reclaim pool is released first)
     rt = {"note": "skipped (--skip-realtime)"}
-    if world > 1:
-        rt = {"note": "measured in the N=1 run (one online tenant per node instance)"}
+    c4 = None
+    if world > 1 and not args.skip_realtime and not args.profile_mode:
+        del gate
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        rt = _guarded("online_realtime_c5", lambda: c5_instances(torch, dist, gpu, rank, world, args))
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        c4 = _guarded("c4_tp_group", lambda: c4_tp(torch, dist, gpu, rank, world, args))
     elif not args.skip_realtime and not args.profile_mode:
         del gate
         gc.collect()
@@ -805,6 +857,7 @@ def run_valve(args, rank, world, dist):
         "ttft_delta_pct": rt.get("ttft_delta_pct"),
         "tpot_delta_pct": rt.get("tpot_delta_pct"),
         "online_realtime": rt,
+        "c4_tp_group": c4 if c4 is not None else {"note": "runs at N >= 2 (one process per GPU)"},
         "roofline": {
             "bound": "pcie_d2h",
             "achieved": round(copy_gbs, 2),

@@ -130,9 +130,10 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
                        int* n_pages);
 /* Device phase durations of the last valve_pool_reclaim (ns, %globaltimer): out[0] instance
  * build (snapshot), out[1] selection, out[2] apply; out[3..4] SM cycles of the greedy rounds
- * (argmin, incremental update); out[5..8] apply sub-phases (evicted rows + ranks, report sort,
- * residual release, request-table erase) of the last apply in this process.  Diagnostics. */
-int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[9]);
+ * (argmin, incremental update); out[5..8] apply sub-phases (evicted rows + ranks, report order,
+ * residual release, request-table erase), out[9..11] (validation, slot collection, per-handle
+ * ranks) of the last apply in this process.  Diagnostics. */
+int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[12]);
 int valve_pool_last_reclaim(const valve_pool* p, int* handles, int64_t* evicted, int* inv_off,
                             int64_t* inv_pages, int* inv_phys, int* inv_blk, int cap_h, int cap_ev,
                             int cap_pages);

@@ -26,7 +26,7 @@ static_assert(kSmemTuples * 20 <= 160 * 1024, "sort smem");
 static_assert((1024 + 3 * 8192 + 6 * 2048) * 4 <= 160 * 1024, "apply fast-path smem");  // key 8 + pay 4 + cursors 4 + segment 4
 
 __device__ long long g_greedy_cycles[2];  // diagnostics: argmin / update cycles of the last run
-__device__ long long g_apply_ns[6];       // diagnostics: apply_core phase stamps of the last run
+__device__ long long g_apply_ns[10];       // diagnostics: apply_core phase stamps of the last run
 
 // Ref lists of instance handle i: CSR (off) or fixed stride with counts (cnt), the stride slot
 // being i itself or map[i] (the fused reclaim lays rows out by handle id: map = instance ids).
@@ -579,6 +579,7 @@ __device__ __forceinline__ void warp_sort_asc(uint64_t* key, int* pay, int n, in
 __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, unsigned char* smem) {
   __shared__ int s_bad, s_nt, s_freed;
   if (threadIdx.x == 0) {
+    g_apply_ns[5] = (long long)globaltimer_ns();
     s_bad = k;
     s_nt = 0;
     s_freed = 0;
@@ -592,6 +593,7 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
   }
   __syncthreads();
   const int b = s_bad;
+  if (threadIdx.x == 0) g_apply_ns[6] = (long long)globaltimer_ns();
   if (threadIdx.x == 0 && b < k) {
     const int h = ids[b];
     if (h < 0 || h >= P.H) set_err(P, kErrOutOfRange, kDetApplyRange, h);
@@ -645,6 +647,7 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
       P.slot_blk[p] = -1;
     }
     __syncthreads();
+    if (threadIdx.x == 0) g_apply_ns[7] = (long long)globaltimer_ns();
     int r_first[kPer], r_wr[kPer];
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
@@ -675,6 +678,7 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
       }
     }
     __syncthreads();
+    if (threadIdx.x == 0) g_apply_ns[8] = (long long)globaltimer_ns();
 #pragma unroll
     for (int j = 0; j < kPer; ++j)
       if (r_first[j] >= 0)

@@ -919,7 +919,7 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
   });
 }
 
-int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[9]) {
+int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[12]) {
   const int64_t* r = p->mirror->r;
   out[0] = r[4] - r[3];
   out[1] = r[5] - r[4];
@@ -928,12 +928,15 @@ int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[9]) {
   cudaMemcpyFromSymbol(cyc, valve::g_greedy_cycles, sizeof cyc);
   out[3] = cyc[0];
   out[4] = cyc[1];
-  long long an[6] = {0, 0, 0, 0, 0, 0};
+  long long an[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpyFromSymbol(an, valve::g_apply_ns, sizeof an);
   out[5] = an[1] - an[0];  // evicted-row compaction + ranks
-  out[6] = an[2] - an[1];  // report sort + outputs
+  out[6] = an[2] - an[1];  // report order + outputs
   out[7] = an[3] - an[2];  // residual page release
   out[8] = an[4] - an[3];  // request-table erase
+  out[9] = an[6] - an[5];  // validation of the pick
+  out[10] = an[7] > an[6] ? an[7] - an[6] : 0;  // slot collection + clear (fast path)
+  out[11] = an[8] > an[7] ? an[8] - an[7] : 0;  // per-handle ranks + pairs (fast path)
   return VALVE_OK;
 }
 

@@ -1348,7 +1348,7 @@ class _Clocks:
 
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,power.draw",
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,power.draw,temperature.gpu,temperature.memory",
                  "--format=csv,noheader,nounits", "-lms", "500"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
@@ -1358,10 +1358,14 @@ class _Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            try:
-                self.rows.append(tuple(float(x) for x in line.split(",")))
-            except ValueError:
-                pass
+            vals = []
+            for x in line.split(","):
+                try:
+                    vals.append(float(x))
+                except ValueError:  # "[N/A]" on boards without a memory sensor
+                    vals.append(float("nan"))
+            if len(vals) >= 2 and vals[0] == vals[0]:
+                self.rows.append(tuple(vals))
 
     def __exit__(self, *a):
         if self.proc:
@@ -1376,8 +1380,13 @@ class _Clocks:
             return None
         sm = sorted(r[0] for r in self.rows)
         pw = sorted(r[1] for r in self.rows)
-        return {"sm_mhz_median": sm[len(sm) // 2], "sm_mhz_min": sm[0], "power_w_median": pw[len(pw) // 2],
-                "power_w_max": pw[-1], "samples": len(sm)}
+        out = {"sm_mhz_median": sm[len(sm) // 2], "sm_mhz_min": sm[0], "power_w_median": pw[len(pw) // 2],
+               "power_w_max": pw[-1], "samples": len(sm)}
+        for i, key in ((2, "gpu_temp_c"), (3, "mem_temp_c")):
+            v = sorted(r[i] for r in self.rows if len(r) > i and r[i] == r[i])
+            if v:
+                out[key + "_median"], out[key + "_max"] = v[len(v) // 2], v[-1]
+        return out
 
 
 def _med_runs(dicts):
@@ -1459,9 +1468,14 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
     runs = {"solo": solos, "colo": colos, **{pol.replace("+", "_"): [r] for pol, r in extra.items()}}
     if log_dir:
         os.makedirs(log_dir, exist_ok=True)
+        import json
+
         for name, rs in runs.items():
             for i, r in enumerate(rs):
                 r.log.write_jsonl(os.path.join(log_dir, f"{name}{i}.jsonl"))
+                with open(os.path.join(log_dir, f"{name}{i}_steps.json"), "w") as f:  # per-step device times
+                    json.dump({"decode_gpu_us": [round(x, 1) for x in r.decode_gpu_us],
+                               "decode_iter_us": r.decode_iter_us, "prefill_us": r.prefill_us}, f)
 
     base_ttft, base_tpot = _med_runs([s.ttft_us for s in solos]), _med_runs([s.tpot_us for s in solos])
     even, odd = solos[0::2], solos[1::2]

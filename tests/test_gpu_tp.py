@@ -173,3 +173,26 @@ def test_member_waits_for_leader_raise_and_own_quiesce():
     torch.cuda.ExternalStream(leader.stream).synchronize()
     member.cancel_work()
     off.synchronize()
+
+
+def test_c4_harness_two_ranks(tmp_path):
+    """C4 harness end to end with two ranks (sharing the box's GPU(s)): the TP=2 online group
+    steps in lockstep, the leader's busy edges raise the group gate, every rank's offline pass
+    quiesces and resumes, and the paired report comes back from the leader."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    out = tmp_path / "c4.json"
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+                        os.path.join(ROOT, "tools", "c4_tp.py"), "--tp", "2", "--layers", "2", "--horizon", "6",
+                        "--handles", "16", "--ctx", "512", "--out", str(out)],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads((tmp_path / "c4_g0.json").read_text())
+    assert d["group"] == [0, 1] and d["pairs"] > 0
+    assert d["group_quiesce_us"]["n"] > 0 and d["disables"][0] > 0
+    assert all(v["offline_gb"][0] > 0 for v in d["per_rank_offline"].values())  # both ranks harvested

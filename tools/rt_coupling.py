@@ -18,7 +18,7 @@ from paper_2604_07874_b200 import api as A  # noqa: E402
 from paper_2604_07874_b200 import realtime as RT  # noqa: E402
 
 
-def main(gap_ms=200.0, repeats=12, iters=24, B=24, ctx=3000, spread=False):
+def main(gap_ms=200.0, repeats=12, iters=24, B=24, ctx=3000, spread="low"):
     import pynvml
 
     pynvml.nvmlInit()
@@ -39,7 +39,10 @@ def main(gap_ms=200.0, repeats=12, iters=24, B=24, ctx=3000, spread=False):
     S = pool.handle_size_pages()
     # contiguous online slots, or the same count spread over the whole 128 GiB page store (the
     # colocated runs' online pages sit in reclaimed handles all over the pool)
-    slots = list(range(0, 128 * S)) if not spread else [(i * 8 + i // 128) % (1024 * S) for i in range(128 * S)]
+    n = 128 * S
+    slots = {"low": list(range(0, n)), "high": list(range(1024 * S - n, 1024 * S)),
+             "mid": list(range(448 * S, 448 * S + n)),
+             "spread": [(i * 8 + i // 128) % (1024 * S) for i in range(n)]}[spread]
     npg = -(-ctx // 16)
     tables = [slots[b * npg:(b + 1) * npg] for b in range(B)]
     model.decode([1] * B, [t[-1] for t in tables], [ctx] * B, tables, slots[-1])
@@ -47,7 +50,7 @@ def main(gap_ms=200.0, repeats=12, iters=24, B=24, ctx=3000, spread=False):
     off, gst = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     gate, ggate = A.Gate(0), A.Gate(0)
     gate.attach_peers([ggate])
-    configs = [("idle", -1, -1), ("gemm64+decode16", 16, 64)]
+    configs = [("idle", -1, -1)]
     gen = 0
     gi = 0
     for name, dctas, gctas in configs:
@@ -93,4 +96,4 @@ def main(gap_ms=200.0, repeats=12, iters=24, B=24, ctx=3000, spread=False):
 
 if __name__ == "__main__":
     main(float(sys.argv[1]) if len(sys.argv) > 1 else 200.0, int(sys.argv[2]) if len(sys.argv) > 2 else 12,
-         spread=len(sys.argv) > 3 and sys.argv[3] == "spread")
+         spread=sys.argv[3] if len(sys.argv) > 3 else "low")

@@ -65,7 +65,7 @@ def parse():
                     help="copy CTAs: 8 already saturate the link (tools/copy_sweep.py); fewer CTAs keep fewer "
                          "bytes queued on PCIe ahead of the next decision's small host-mapped writes")
     ap.add_argument("--copy-threads", type=int, default=512)
-    ap.add_argument("--tma", type=int, default=0)
+    ap.add_argument("--tma", type=int, default=1, help="1: cp.async.bulk copy through shared memory, 0: LDG/STG")
     ap.add_argument("--seed", type=int, default=2604)
     ap.add_argument("--skip-realtime", action="store_true", help="skip the measured TTFT/TPOT run")
     ap.add_argument("--skip-fanout", action="store_true", help="skip the same-device TP fan-out sweep")
@@ -854,8 +854,11 @@ def run_valve(args, rank, world, dist):
         "tp_fanout_same_device": fanout,
         "policy_contrast_recompute": contrast,
         "c3_weight_pages": c3,
-        "ttft_delta_pct": rt.get("ttft_delta_pct"),
-        "tpot_delta_pct": rt.get("tpot_delta_pct"),
+        "ttft_delta_pct": (rt.get("valve") or {}).get("ttft_delta_pct", rt.get("ttft_delta_pct_max")),
+        "tpot_delta_pct": (rt.get("valve") or {}).get("tpot_delta_pct", rt.get("tpot_delta_pct_max")),
+        "aa_noise_ttft_pct": rt.get("aa_noise_ttft_pct"),
+        "aa_noise_tpot_pct": rt.get("aa_noise_tpot_pct"),
+        "shortfall_to_first_online_write_us": (rt.get("valve") or {}).get("shortfall_to_first_write_us"),
         "online_realtime": rt,
         "c4_tp_group": c4 if c4 is not None else {"note": "runs at N >= 2 (one process per GPU)"},
         "roofline": {
@@ -868,7 +871,7 @@ def run_valve(args, rank, world, dist):
             "traffic_source": traffic.get("source"),
             "peak_source": "pinned cudaMemcpy D2H measured in this run (the copy's true roofline; "
                            "HBM is ~110x faster)",
-            "kernel": "k_reclaim_copy",
+            "kernel": "k_reclaim_copy_tma" if args.tma else "k_reclaim_copy",
             "algorithmic_bytes_per_launch": round(statistics.mean(stats["bytes"])),
             "hbm": {"achieved": round(copy_gbs, 2), "peak": HBM_PEAK, "unit": "GB/s",
                     "frac": round(copy_gbs / HBM_PEAK, 5), "peak_source": HBM_PEAK_SOURCE},

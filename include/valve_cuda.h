@@ -145,7 +145,8 @@ typedef struct {
   int64_t chunk_bytes;      /* work unit; 0 = default (64 KiB) */
   double rate_bytes_per_s;  /* rate bound; <= 0 = unbounded */
   int64_t burst_bytes;      /* token-bucket depth for the rate bound */
-  int use_tma;              /* 1 = stage chunks through shared memory with cp.async.bulk */
+  int use_tma;              /* 1 (default) = stage chunks through shared memory with cp.async.bulk
+                               (one elected thread per CTA); 0 = register-staged LDG/STG kernel */
   void* trace;              /* optional device uint64[n_chunks]: %globaltimer issue time of each
                                chunk (rate-bound tests); NULL = off */
 } valve_copy_params;

@@ -75,6 +75,41 @@ __device__ __forceinline__ void publish_all(const CopyArgs& A) {
     atomicMax(A.landed, A.wave_base + (unsigned long long)A.n_waves);
 }
 
+// Source offset in the page store, destination offset and length of chunk c of the report:
+// page-major (page = c / cpp) or wave-major (wave = c / n_pages: bytes [wave * chunk, ...) of
+// every page, so the landed counter can publish a wave once all pages' wave bytes are read), or
+// located by the chunk prefix when evicted requests have their own page sizes.
+__device__ __forceinline__ void locate(const CopyArgs& A, long long c, int64_t cpp, int64_t& src, int64_t& dst,
+                                       int64_t& len) {
+  if (A.ev_cbase) {  // variable page sizes: locate the evicted request by its chunk prefix
+    int lo = 0, hi = A.n_ev - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (A.ev_cbase[mid] <= c) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t pb = A.ev_pbytes[lo];
+    const int64_t cp = (pb + A.chunk_bytes - 1) / A.chunk_bytes;
+    const int64_t local = c - A.ev_cbase[lo];
+    const int64_t pg = local / cp, off = (local % cp) * A.chunk_bytes;
+    src = (int64_t)A.phys[A.inv_off[lo] + pg] * A.slot_bytes + off;
+    dst = A.ev_base[lo] + pg * pb + off;
+    len = min(A.chunk_bytes, pb - off);
+    return;
+  }
+  int64_t page, off;
+  if (A.wave_major) {
+    page = c % A.n_pages;
+    off = (c / A.n_pages) * A.chunk_bytes;
+  } else {
+    page = c / cpp;
+    off = (c % cpp) * A.chunk_bytes;
+  }
+  src = (int64_t)A.phys[page] * A.slot_bytes + off;
+  dst = page * A.page_bytes + off;
+  len = min(A.chunk_bytes, A.page_bytes - off);
+}
+
 }  // namespace
 
 constexpr int kVec = 8;
@@ -113,33 +148,9 @@ __global__ void __launch_bounds__(512) k_reclaim_copy(CopyArgs A) {
       s_chunk = c;
       prev = c;
       if (c < n_chunks) {
-        if (A.ev_cbase) {  // variable page sizes: locate the evicted request by its chunk prefix
-          int lo = 0, hi = A.n_ev - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (A.ev_cbase[mid] <= c) lo = mid;
-            else hi = mid - 1;
-          }
-          const int64_t pb = A.ev_pbytes[lo];
-          const int64_t cp = (pb + A.chunk_bytes - 1) / A.chunk_bytes;
-          const int64_t local = c - A.ev_cbase[lo];
-          const int64_t pg = local / cp, off = (local % cp) * A.chunk_bytes;
-          s_src = (int64_t)A.phys[A.inv_off[lo] + pg] * A.slot_bytes + off;
-          s_dst = A.ev_base[lo] + pg * pb + off;
-          s_len = min(A.chunk_bytes, pb - off);
-        } else {
-          int64_t page, off;
-          if (A.wave_major) {
-            page = c % A.n_pages;
-            off = (c / A.n_pages) * A.chunk_bytes;
-          } else {
-            page = c / cpp;
-            off = (c % cpp) * A.chunk_bytes;
-          }
-          s_src = (int64_t)A.phys[page] * A.slot_bytes + off;
-          s_dst = page * A.page_bytes + off;
-          s_len = min(A.chunk_bytes, A.page_bytes - off);
-        }
+        int64_t so, d, l;
+        locate(A, c, cpp, so, d, l);
+        s_src = so, s_dst = d, s_len = l;
         pace(A, s_len, c);
       }
     }
@@ -224,8 +235,10 @@ __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// One elected thread per CTA drives the bulk engine; chunks of kTmaChunk bytes are claimed
-// in CTA-sized batches from the cursor (the pace() bound applies per claim).
+// One elected thread per CTA drives the bulk engine; each claimed chunk (any layout: page-major,
+// wave-major or per-request page sizes) moves in kTmaChunk pieces, and its wave is counted as
+// soon as its last piece has landed in shared memory (its HBM bytes are read), so the landed
+// tickets advance exactly as with the register-staged kernel.
 __global__ void __launch_bounds__(32) k_reclaim_copy_tma(CopyArgs A) {
   extern __shared__ __align__(128) unsigned char sbuf[];  // 2 x kTmaChunk
   __shared__ __align__(8) uint64_t bar[2];
@@ -235,27 +248,31 @@ __global__ void __launch_bounds__(32) k_reclaim_copy_tma(CopyArgs A) {
   mbar_init(&bar[1], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   const int64_t cpp = (A.page_bytes + A.chunk_bytes - 1) / A.chunk_bytes;
+  const long long n_chunks = A.ev_cbase ? A.ev_cbase[A.n_ev] : A.n_chunks;
   unsigned phase[2] = {0, 0};
   int buf = 0;
   for (;;) {
     const long long c = (long long)atomicAdd(A.cursor, 1ull);
-    if (c >= A.n_chunks) break;
-    const int64_t page = c / cpp;
-    const int64_t off0 = (c % cpp) * A.chunk_bytes;
-    const int64_t len = min(A.chunk_bytes, A.page_bytes - off0);
+    if (c >= n_chunks) break;
+    int64_t so, d, len;
+    locate(A, c, cpp, so, d, len);
     pace(A, len, c);
-    const uint8_t* src = A.pages + (int64_t)A.phys[page] * A.slot_bytes + off0;
-    uint8_t* dst = A.dst + page * A.page_bytes + off0;
+    const uint8_t* src = A.pages + so;
+    uint8_t* dst = A.dst + d;
     for (int64_t o = 0; o < len; o += kTmaChunk) {
       const unsigned bytes = (unsigned)min((int64_t)kTmaChunk, len - o);
-      unsigned char* s = sbuf + buf * kTmaChunk;
+      unsigned char* sm = sbuf + buf * kTmaChunk;
       bulk_wait_read_le1();  // the store that last read this buffer has drained
       mbar_expect_tx(&bar[buf], bytes);
-      bulk_g2s(s, src + o, bytes, &bar[buf]);
+      bulk_g2s(sm, src + o, bytes, &bar[buf]);
       mbar_wait(&bar[buf], phase[buf]);
       phase[buf] ^= 1;
-      bulk_s2g(dst + o, s, bytes);
+      bulk_s2g(dst + o, sm, bytes);
       buf ^= 1;
+    }
+    if (A.wave_major) {  // every byte of this chunk has been read out of HBM
+      const unsigned w = (unsigned)(c / A.n_pages);
+      if (atomicAdd(&A.wave_done[w], 1u) + 1u == (unsigned)A.n_pages) publish_waves(A, (unsigned)A.n_pages);
     }
   }
   bulk_wait_all();

@@ -470,6 +470,8 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
   } else {
     build_instance_index(n, R, rref, m, cost, marg_g, qoff, qcnt, qh, ev);
     greedy_cta(n, hid_g, R, rref, cost, k, marg_g, taken_g, ev, qoff, qh, out);
+    __syncthreads();
+    for (int r = threadIdx.x; r < m; r += blockDim.x) ev[r] = 0;  // apply re-marks rows
   }
 }
 
@@ -608,11 +610,12 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
   // position, count); sorting the few pairs by (request rank, handle position) and a scan of
   // their counts gives every page its report position without sorting the pages.
   constexpr int kFastT = 8192, kFastB = 1024, kPairCap = 2048, kPer = kFastT / kNT;
-  const bool fast = (int64_t)b * P.S <= kFastT && b <= kFastB;
+  // packed per-slot key (row << 16 | lid << 8 | slot) needs rows < 2^16 and S <= 256
+  const bool fast = (int64_t)b * P.S <= kFastT && b <= kFastB && P.R < 65535 && P.S <= 256;
   int* hs = reinterpret_cast<int*>(smem);  // [kFastB] chosen handles, ascending
   int* trow = hs + kFastB;                 // [kFastT] slot tuples: row (-1 = empty slot)
-  int* tlid = trow + kFastT;               //   logical id inside the handle
-  int* tpid = tlid + kFastT;               //   pair id (on the row's first slot of the handle)
+  int* tkey = trow + kFastT;               //   row << 16 | logical id << 8 | slot (rank key)
+  int* tpid = tkey + kFastT;               //   pair id (on the row's first slot of the handle)
   int* prow = tpid + kFastT;               // [kPairCap] pair: row
   int* phi = prow + kPairCap;              //   handle position in ascending order
   int* pcnt = phi + kPairCap;              //   pages of the row on that handle
@@ -635,9 +638,10 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
       const int64_t p = (int64_t)hs[hi] * P.S + (idx - hi * P.S);
       const int row = P.slot_row[p];
       trow[idx] = row;
+      tkey[idx] = -1;  // empty: row field 0xffff never matches a row < 65535
       if (row < 0) continue;
       const int blk = P.slot_blk[p];
-      tlid[idx] = P.slot_lid[p];
+      tkey[idx] = (row << 16) | (P.slot_lid[p] << 8) | (idx - hi * P.S);
       P.s_pay[idx] = blk;
       atomicAdd(&s_nt, 1);
       P.bt[(int64_t)row * P.P + blk] = P.quarantine;  // quarantine remap
@@ -648,41 +652,109 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
     }
     __syncthreads();
     if (threadIdx.x == 0) g_apply_ns[7] = (long long)globaltimer_ns();
-    int r_first[kPer], r_wr[kPer];
+    if (P.S <= 64) {
+      // one warp per handle: bitonic sort of its <= 64 packed keys (row, lid, slot) in registers
+      // (position p = lane + 32 * i holds a_i), then each page's rank inside its row's segment
+      // = p - segment start (ballots of the segment starts); the segment start owns the pair
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      const unsigned le = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);  // lanes <= me
+      for (int hi = wid; hi < b; hi += nw) {
+        const int base = hi * P.S;
+        unsigned a0 = lane < P.S ? (unsigned)tkey[base + lane] : 0xFFFFFFFFu;
+        unsigned a1 = lane + 32 < P.S ? (unsigned)tkey[base + lane + 32] : 0xFFFFFFFFu;
 #pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int idx = threadIdx.x + j * kNT;
-      r_first[j] = -1;
-      const int row = idx < nslot ? trow[idx] : -1;
-      if (row < 0) continue;
-      const int base = (idx / P.S) * P.S, s = idx - base;
-      const int lid = tlid[idx];
-      int cnt = 0, wr = 0, first = s;
-      for (int q = 0; q < P.S; ++q) {
-        if (trow[base + q] != row) continue;
-        ++cnt;
-        const int lq = tlid[base + q];
-        wr += lq < lid || (lq == lid && q < s);
-        first = min(first, q);
+        for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+          for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {  // k == 64: partner is the other register of the same lane, ascending
+              const unsigned lo = min(a0, a1), hi2 = max(a0, a1);
+              a0 = lo, a1 = hi2;
+            } else {
+              const unsigned b0 = __shfl_xor_sync(kFull, a0, j), b1 = __shfl_xor_sync(kFull, a1, j);
+              const bool lower = (lane & j) == 0;
+              a0 = (lower == ((lane & k) == 0)) ? min(a0, b0) : max(a0, b0);
+              a1 = (lower == (((lane + 32) & k) == 0)) ? min(a1, b1) : max(a1, b1);
+            }
+          }
+        }
+        const unsigned r0 = a0 >> 16, r1 = a1 >> 16;
+        unsigned p0 = __shfl_up_sync(kFull, r0, 1), p1 = __shfl_up_sync(kFull, r1, 1);
+        const unsigned tail0 = __shfl_sync(kFull, r0, 31);
+        if (lane == 0) p0 = ~r0, p1 = tail0;
+        const unsigned m0 = __ballot_sync(kFull, p0 != r0), m1 = __ballot_sync(kFull, p1 != r1);
+        // segment start / next start of each position
+        const int st0 = 31 - __clz(m0 & le);  // lane 0 is always a start
+        const unsigned mm1 = m1 & le;
+        const int st1 = mm1 ? 32 + 31 - __clz(mm1) : 31 - __clz(m0);
+        const unsigned n0m = m0 & ~le, n1m = m1 & ~le;
+        const int nx0 = n0m ? __ffs(n0m) - 1 : (m1 ? 32 + __ffs(m1) - 1 : 64);
+        const int nx1 = n1m ? 32 + __ffs(n1m) - 1 : 64;
+        int pid0 = -1, pid1 = -1;
+        const bool v0 = r0 != 0xFFFFu, v1 = r1 != 0xFFFFu;  // 0xffff: empty slot
+        if (v0 && st0 == lane) {
+          pid0 = atomicAdd(&s_np, 1);
+          if (pid0 < kPairCap) prow[pid0] = (int)r0, phi[pid0] = hi, pcnt[pid0] = nx0 - st0;
+          if (atomicExch(&P.s_ev[r0], 1) == 0) {
+            const int e = atomicAdd(&s_ne, 1);
+            if (e < kPairCap) sev[e] = (int)r0;
+          }
+        }
+        if (v1 && st1 == lane + 32) {
+          pid1 = atomicAdd(&s_np, 1);
+          if (pid1 < kPairCap) prow[pid1] = (int)r1, phi[pid1] = hi, pcnt[pid1] = nx1 - st1;
+          if (atomicExch(&P.s_ev[r1], 1) == 0) {
+            const int e = atomicAdd(&s_ne, 1);
+            if (e < kPairCap) sev[e] = (int)r1;
+          }
+        }
+        // each page takes its segment start's pair id (start lane / register by position)
+        const int q0 = __shfl_sync(kFull, pid0, st0 & 31), q0b = __shfl_sync(kFull, pid1, st0 & 31);
+        const int q1 = __shfl_sync(kFull, pid0, st1 & 31), q1b = __shfl_sync(kFull, pid1, st1 & 31);
+        if (v0) P.s_key[base + (a0 & 0xFFu)] = ((uint64_t)(uint32_t)(st0 < 32 ? q0 : q0b) << 32) | (uint32_t)(lane - st0);
+        if (v1) P.s_key[base + (a1 & 0xFFu)] = ((uint64_t)(uint32_t)(st1 < 32 ? q1 : q1b) << 32) | (uint32_t)(lane + 32 - st1);
       }
-      r_first[j] = base + first;
-      r_wr[j] = wr;
-      if (first == s) {  // the row's first slot on this handle owns the pair
-        const int pid = atomicAdd(&s_np, 1);
-        tpid[idx] = pid;
-        if (pid < kPairCap) prow[pid] = row, phi[pid] = base / P.S, pcnt[pid] = cnt;
-        if (atomicExch(&P.s_ev[row], 1) == 0) {
-          const int e = atomicAdd(&s_ne, 1);
-          if (e < kPairCap) sev[e] = row;
+      __syncthreads();
+      if (threadIdx.x == 0) g_apply_ns[8] = (long long)globaltimer_ns();
+    } else {
+      int r_first[kPer], r_wr[kPer];
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int idx = threadIdx.x + j * kNT;
+        r_first[j] = -1;
+        const int row = idx < nslot ? trow[idx] : -1;
+        if (row < 0) continue;
+        const int base = (idx / P.S) * P.S, s = idx - base;
+        // rank among the row's pages on this handle by (lid, slot): one packed key per slot, so the
+        // scan is branch-free (empty slots hold key 0xffffffff and never match)
+        const unsigned ks = (unsigned)tkey[idx], rk = (unsigned)row;
+        int cnt = 0, wr = 0, first = s;
+#pragma unroll 8
+        for (int q = 0; q < P.S; ++q) {
+          const unsigned kq = (unsigned)tkey[base + q];
+          const bool same = (kq >> 16) == rk;
+          cnt += same;
+          wr += same && kq < ks;
+          first = same && q < first ? q : first;
+        }
+        r_first[j] = base + first;
+        r_wr[j] = wr;
+        if (first == s) {  // the row's first slot on this handle owns the pair
+          const int pid = atomicAdd(&s_np, 1);
+          tpid[idx] = pid;
+          if (pid < kPairCap) prow[pid] = row, phi[pid] = base / P.S, pcnt[pid] = cnt;
+          if (atomicExch(&P.s_ev[row], 1) == 0) {
+            const int e = atomicAdd(&s_ne, 1);
+            if (e < kPairCap) sev[e] = row;
+          }
         }
       }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) g_apply_ns[8] = (long long)globaltimer_ns();
+      __syncthreads();
+      if (threadIdx.x == 0) g_apply_ns[8] = (long long)globaltimer_ns();
 #pragma unroll
-    for (int j = 0; j < kPer; ++j)
-      if (r_first[j] >= 0)
-        P.s_key[threadIdx.x + j * kNT] = ((uint64_t)(uint32_t)tpid[r_first[j]] << 32) | (uint32_t)r_wr[j];
+      for (int j = 0; j < kPer; ++j)
+        if (r_first[j] >= 0)
+          P.s_key[threadIdx.x + j * kNT] = ((uint64_t)(uint32_t)tpid[r_first[j]] << 32) | (uint32_t)r_wr[j];
+    }
     if (s_np > kPairCap || s_ne > kPairCap) {
       // too many pairs for the on-chip report: compact the tuples for the general sort below
       __shared__ int s_cmp;
@@ -694,7 +766,7 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
         const int hi = idx / P.S;
         const int pos = atomicAdd(&s_cmp, 1);
         P.s_qh[pos] = row;
-        P.s_rref[pos] = hs[hi] * P.S + tlid[idx];
+        P.s_rref[pos] = hs[hi] * P.S + ((tkey[idx] >> 8) & 0xff);
         P.s_tphys[pos] = hs[hi] * P.S + (idx - hi * P.S);
         P.s_tblk[pos] = P.s_pay[idx];
       }
@@ -789,7 +861,7 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
       const uint64_t kv = P.s_key[idx];
       const int pos = ppos[kv >> 32] + (int)(uint32_t)kv;
       const int hi = idx / P.S, h = hs[hi];
-      P.res_pages[pos] = (int64_t)h * P.S + tlid[idx];
+      P.res_pages[pos] = (int64_t)h * P.S + ((tkey[idx] >> 8) & 0xff);
       P.res_phys[pos] = h * P.S + (idx - hi * P.S);
       P.res_blk[pos] = P.s_pay[idx];
     }
@@ -1045,8 +1117,7 @@ __device__ void reclaim_body(const PoolDev& P, int k, int mode, int64_t t, unsig
     fifo_core(n, P.s_hid, P.s_hmap, k, P.s_pick);
   } else {
     greedy_select(n, P.s_hid, R, P.s_rref, P.R, P.row_cost, k, P.s_marg, P.s_taken, P.s_ev,
-                  P.s_qoff, P.s_qcnt, P.s_qh, P.s_pick, smem);
-    for (int r = threadIdx.x; r < P.R; r += blockDim.x) P.s_ev[r] = 0;  // apply re-marks rows
+                  P.s_qoff, P.s_qcnt, P.s_qh, P.s_pick, smem);  // leaves s_ev zeroed
   }
   __syncthreads();
   if (threadIdx.x == 0) P.mirror->r[5] = (int64_t)globaltimer_ns();

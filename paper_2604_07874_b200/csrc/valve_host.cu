@@ -980,7 +980,7 @@ void valve_copy_params_default(valve_copy_params* c) {
   c->chunk_bytes = 65536;
   c->rate_bytes_per_s = 0;
   c->burst_bytes = 0;
-  c->use_tma = 0;
+  c->use_tma = 1;  // shared-memory staged bulk copies (same link rate as the register-staged kernel)
   c->trace = nullptr;
 }
 
@@ -1029,15 +1029,14 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
     A.t_first = S.ctr + 1;
     A.t_last = S.ctr + 2;
     // landed tickets: wave-major order (one wave = the same chunk_bytes of every page) when the
-    // page size is uniform and the SM kernel runs; otherwise the whole copy is one wave
-    A.wave_major = (!custom && !c.use_tma && cpp <= valve_pool::kMaxWaves && n_pages > 0) ? 1 : 0;
+    // page size is uniform; otherwise the whole copy is one wave
+    A.wave_major = (!custom && cpp <= valve_pool::kMaxWaves && n_pages > 0) ? 1 : 0;
     A.n_waves = n_pages == 0 ? 0 : (A.wave_major ? (int)cpp : 1);
     A.wave_done = S.waves;
     A.wave_next = S.waves + valve_pool::kMaxWaves;
     A.ctas_done = S.waves + valve_pool::kMaxWaves + 1;
     A.landed = p->d_landed;
     A.wave_base = p->waves_issued;
-    if (c.trace && c.use_tma) fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: trace needs the SM copy kernel");
     // the copy runs on its own stream after the report exists and works from its own snapshot
     // of it; bookkeeping and the next decision proceed on the pool stream meanwhile
     // the snapshot runs on the plan stream, so a copy queued behind a running one does not hold
@@ -1069,7 +1068,7 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
     }
     ck(cudaEventRecord(S.ev0, p->copy_stream), "event");
     if (A.n_chunks > 0) {
-      if (c.use_tma && !custom) {
+      if (c.use_tma) {
         k_reclaim_copy_tma<<<c.ctas, 32, 2 * 32768, p->copy_stream>>>(A);
       } else {
         k_reclaim_copy<<<c.ctas, c.threads, 0, p->copy_stream>>>(A);

@@ -363,7 +363,7 @@ def _expected_images_var(oracle_c, res, sizes, default):
 @pytest.mark.parametrize("engine,kw", [
     ("sm", dict(ctas=6, chunk_bytes=8192)),
     ("sm", dict(ctas=2, chunk_bytes=65536)),
-    ("sm", dict(ctas=4, use_tma=1, chunk_bytes=8192)),  # variable sizes take the LDG/STG kernel
+    ("sm", dict(ctas=4, use_tma=1, chunk_bytes=8192)),  # variable sizes through the bulk-copy kernel
     ("ce", {}),
 ])
 def test_weight_pages_fill_whole_slots(oracle_c, engine, kw):

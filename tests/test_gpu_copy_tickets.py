@@ -33,7 +33,10 @@ def _slot_tensor(torch, pool):
     return torch.as_tensor(_Arr(), device=f"cuda:{pool.device}")
 
 
-def test_tickets_guard_every_wave_against_online_overwrites(oracle_c):
+@pytest.mark.parametrize("use_tma", [0, 1])
+def test_tickets_guard_every_wave_against_online_overwrites(oracle_c, use_tma):
+    """Both copy kernels (register-staged LDG/STG and shared-memory staged cp.async.bulk) publish
+    waves only after the wave's bytes were read out of HBM."""
     torch = pytest.importorskip("torch")
     rng = random.Random(5)
     pool, live = _pool_with_pages(rng, H=48, S=8, slot=65536, page=49152, n_req=80)
@@ -53,7 +56,7 @@ def test_tickets_guard_every_wave_against_online_overwrites(oracle_c):
         torch.cuda.Event(enable_timing=True).record(online)
     online.synchronize()
     # slow enough (0.1 GB/s, ~24 ms) that an early overwrite would certainly beat the copy
-    pool.reclaim_copy_start(buf.ptr, buf.nbytes, A.copy_params(ctas=3, chunk_bytes=chunk,
+    pool.reclaim_copy_start(buf.ptr, buf.nbytes, A.copy_params(ctas=3, chunk_bytes=chunk, use_tma=use_tma,
                                                                  rate_bytes_per_s=1e8, burst_bytes=chunk))
     base, waves, wave_bytes = pool.copy_ticket()
     assert waves == -(-pool.page_bytes // chunk) and wave_bytes == chunk
@@ -94,7 +97,7 @@ def test_tickets_accumulate_across_pipelined_copies(oracle_c):
     b2 = A.HostBuffer(n2 * pool.page_bytes)
     pool.reclaim_copy_start(b2.ptr, b2.nbytes, A.copy_params(ctas=4, chunk_bytes=4096, use_tma=1))
     base2, w2, wb2 = pool.copy_ticket()
-    assert base2 == base1 + w1 and w2 == 1 and wb2 == pool.slot_bytes  # TMA path: one wave
+    assert base2 == base1 + w1 and w2 == -(-pool.page_bytes // 4096) and wb2 == 4096  # TMA: wave-major too
     with pytest.raises(A.InvalidArgument):
         pool.wait_landed(base2 + w2 + 1)
     s = torch.cuda.Stream()

@@ -119,6 +119,14 @@ void table(int H, const std::vector<int>& ks) {
   Population pop;
   pool.online_grow((H + 9) / 10, 0);
   pop.fill(pool);
+#ifdef VALVE_DROPIN
+  // the fused single-call path runs on its own pool + population, so the API-path sequence
+  // (and every number it reports) stays call-for-call identical to the reference build's
+  MemoryPool fpool = make_pool(H, false);
+  Population fpop;
+  fpool.online_grow((H + 9) / 10, 0);
+  fpop.fill(fpool);
+#endif
   // offline_release + offline_reserve of live requests (the re-admission path)
   std::vector<double> rel, res;
   std::vector<std::int64_t> ids;
@@ -146,7 +154,7 @@ void table(int H, const std::vector<int>& ks) {
   for (std::size_t ki = 0; ki < ks.size(); ++ki) {
     const int k = ks[ki];
     std::vector<double> snap, sel, app, tot, fused;
-    std::int64_t pages = 0;
+    std::int64_t pages = 0, pages_all = 0;
     const int reps = 15;
     for (int rep = 0; rep < reps + 2; ++rep) {
       auto a = clk::now();
@@ -164,28 +172,29 @@ void table(int H, const std::vector<int>& ks) {
       }
       pages = 0;
       for (const auto& kv : rr.invalidated_pages) pages += static_cast<std::int64_t>(kv.second.size());
+      pages_all += pages;
       pop.restore(pool, static_cast<int>(rr.handles.size()), rr.evicted_requests);
 #ifdef VALVE_DROPIN
       // the B200 single call: snapshot + Algorithm 1 + apply on the device (costs kept with the rows)
       std::vector<std::int64_t> rq, cs;
-      for (const auto& kv : pop.live) rq.push_back(kv.first), cs.push_back(kv.second.second);
-      valve_detail::check(valve_pool_set_costs(pool.native(), static_cast<int>(rq.size()), rq.data(), cs.data()));
+      for (const auto& kv : fpop.live) rq.push_back(kv.first), cs.push_back(kv.second.second);
+      valve_detail::check(valve_pool_set_costs(fpool.native(), static_cast<int>(rq.size()), rq.data(), cs.data()));
       int nh = 0, ne = 0, np = 0;
       auto e = clk::now();
-      valve_detail::check(valve_pool_reclaim(pool.native(), k, VALVE_SELECT_SELECTIVE, ++pop.t, &nh, &ne, &np));
+      valve_detail::check(valve_pool_reclaim(fpool.native(), k, VALVE_SELECT_SELECTIVE, ++fpop.t, &nh, &ne, &np));
       auto f = clk::now();
       if (rep >= 2) fused.push_back(us(e, f));
       std::vector<int> hs(static_cast<std::size_t>(nh) + 1);
       std::vector<std::int64_t> ev(static_cast<std::size_t>(ne) + 1);
-      valve_detail::check(valve_pool_last_reclaim(pool.native(), hs.data(), ev.data(), nullptr, nullptr, nullptr,
+      valve_detail::check(valve_pool_last_reclaim(fpool.native(), hs.data(), ev.data(), nullptr, nullptr, nullptr,
                                                   nullptr, nh + 1, ne + 1, 0));
       ev.resize(static_cast<std::size_t>(ne));
-      pop.restore(pool, nh, ev);
+      fpop.restore(fpool, nh, ev);
 #endif
     }
-    std::printf("%s{\"k\": %d, \"pages\": %lld, \"snapshot_us\": %.2f, \"select_us\": %.2f, \"apply_us\": %.2f, "
+    std::printf("%s{\"k\": %d, \"pages\": %lld, \"pages_all_reps\": %lld, \"snapshot_us\": %.2f, \"select_us\": %.2f, \"apply_us\": %.2f, "
                 "\"api_total_us\": %.2f",
-                ki ? ", " : "", k, static_cast<long long>(pages), median(snap), median(sel), median(app),
+                ki ? ", " : "", k, static_cast<long long>(pages), static_cast<long long>(pages_all), median(snap), median(sel), median(app),
                 median(tot));
 #ifdef VALVE_DROPIN
     std::printf(", \"fused_us\": %.2f", median(fused));

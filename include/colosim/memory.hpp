@@ -96,19 +96,16 @@ class MemoryPool {
 
   ReclaimInstance snapshot() const {
     int nh = 0, nr = 0;
-    valve_detail::check(valve_pool_snapshot(pool_.get(), nullptr, nullptr, nullptr, nullptr, 0, 0, &nh, &nr));
-    std::vector<int> ids(static_cast<std::size_t>(nh)), off(static_cast<std::size_t>(nh) + 1);
-    std::vector<std::int64_t> mapped(static_cast<std::size_t>(nh)), reqs(static_cast<std::size_t>(nr));
-    valve_detail::check(valve_pool_snapshot(pool_.get(), ids.data(), mapped.data(), off.data(), reqs.data(),
-                                            nh, nr, &nh, &nr));
+    const int *ids = nullptr, *off = nullptr;
+    const std::int64_t *mapped = nullptr, *reqs = nullptr;
+    valve_detail::check(valve_pool_snapshot_view(pool_.get(), &ids, &mapped, &off, &reqs, &nh, &nr));
     ReclaimInstance inst;
     inst.handles.resize(static_cast<std::size_t>(nh));
     for (int i = 0; i < nh; ++i) {
       ReclaimHandle& h = inst.handles[static_cast<std::size_t>(i)];
-      h.id = ids[static_cast<std::size_t>(i)];
-      h.mapped_at = mapped[static_cast<std::size_t>(i)];
-      h.requests.assign(reqs.begin() + off[static_cast<std::size_t>(i)],
-                        reqs.begin() + off[static_cast<std::size_t>(i) + 1]);
+      h.id = ids[i];
+      h.mapped_at = mapped[i];
+      h.requests.assign(reqs + off[i], reqs + off[i + 1]);
     }
     return inst;
   }
@@ -119,21 +116,16 @@ class MemoryPool {
     std::map<std::int64_t, std::vector<std::int64_t>> invalidated_pages;
   };
   ReclaimResult apply_reclaim(const std::vector<int>& handle_ids, SimTime t) {
-    const std::int64_t cap = static_cast<std::int64_t>(total_) * hsz_;
-    std::vector<int> handles(handle_ids.size() + static_cast<std::size_t>(total_) + 1);
-    std::vector<std::int64_t> ev(static_cast<std::size_t>(cap) + 1), pages(static_cast<std::size_t>(cap) + 1);
-    std::vector<int> off(static_cast<std::size_t>(cap) + 2);
     int nh = 0, ne = 0, np = 0;
-    valve_detail::check(valve_pool_apply_reclaim(pool_.get(), handle_ids.data(),
-                                                 static_cast<int>(handle_ids.size()), t, handles.data(), &nh,
-                                                 ev.data(), &ne, off.data(), pages.data(), nullptr, nullptr,
-                                                 static_cast<int>(cap) + 1, static_cast<int>(cap) + 1, &np));
+    const int *handles = nullptr, *off = nullptr;
+    const std::int64_t *ev = nullptr, *pages = nullptr;
+    valve_detail::check(valve_pool_apply_reclaim_view(pool_.get(), handle_ids.data(),
+                                                      static_cast<int>(handle_ids.size()), t, &handles, &nh, &ev,
+                                                      &ne, &off, &pages, &np));
     ReclaimResult r;
-    r.handles.assign(handles.begin(), handles.begin() + nh);
-    r.evicted_requests.assign(ev.begin(), ev.begin() + ne);
-    for (int i = 0; i < ne; ++i)
-      r.invalidated_pages[ev[static_cast<std::size_t>(i)]].assign(
-          pages.begin() + off[static_cast<std::size_t>(i)], pages.begin() + off[static_cast<std::size_t>(i) + 1]);
+    r.handles.assign(handles, handles + nh);
+    r.evicted_requests.assign(ev, ev + ne);
+    for (int i = 0; i < ne; ++i) r.invalidated_pages[ev[i]].assign(pages + off[i], pages + off[i + 1]);
     return r;
   }
 

@@ -104,6 +104,14 @@ int valve_pool_apply_reclaim(valve_pool* p, const int* ids, int k, int64_t t, in
                              int* n_handles, int64_t* evicted, int* n_evicted, int* inv_off,
                              int64_t* inv_pages, int* inv_phys, int* inv_blk, int cap_ev,
                              int cap_pages, int* n_pages);
+/* Zero-copy forms of snapshot / apply_reclaim for C++ callers (the include/colosim drop-in): the
+ * results land in pinned staging owned by the pool (one DMA each, no pageable copies) and the
+ * returned pointers stay valid until the next snapshot / apply / last_reclaim call on the pool. */
+int valve_pool_snapshot_view(valve_pool* p, const int** ids, const int64_t** mapped_at, const int** off,
+                             const int64_t** reqs, int* nh, int* nr);
+int valve_pool_apply_reclaim_view(valve_pool* p, const int* ids, int k, int64_t t, const int** handles,
+                                  int* n_handles, const int64_t** evicted, int* n_evicted, const int** inv_off,
+                                  const int64_t** inv_pages, int* n_pages);
 int valve_pool_handle_state(const valve_pool* p, int handle, int* state);      /* memory.hpp:73 */
 int valve_pool_handle_mapped_at(const valve_pool* p, int handle, int64_t* t);  /* memory.hpp:74 */
 int valve_pool_check_invariants(const valve_pool* p);                          /* memory.hpp:78 */

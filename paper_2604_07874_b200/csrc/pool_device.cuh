@@ -20,6 +20,7 @@ __device__ __forceinline__ void publish(const PoolDev& P) {
     P.mirror->n_online = P.hdr->n_online;
     P.mirror->n_offline = P.hdr->n_offline;
     __threadfence_system();
+    P.mirror->done_seq = P.seq;  // after the fence: the host reads the results once it sees this
   }
 }
 

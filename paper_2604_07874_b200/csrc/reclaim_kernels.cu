@@ -1154,11 +1154,8 @@ __global__ void __launch_bounds__(kNT) k_reclaim_fused(PoolDev P, int k, int mod
   if (!s_last) return;
   __threadfence();
   if (threadIdx.x == 0) *P.ticket = 0;  // ready for the next launch (stream-ordered)
-  reclaim_body(P, k, mode, t, smem);
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    P.mirror->done_seq = seq;
-  }
+  reclaim_body(P, k, mode, t, smem);  // ends in publish(): stores P.seq (== seq) into the mirror
+  (void)seq;
 }
 
 // ---------------------------------------------------- selection over host instances

@@ -122,6 +122,8 @@ struct valve_pool {
   cudaStream_t stream = nullptr;
   PoolDev d{};
   Mirror* mirror = nullptr;  // pinned host
+  uint8_t* hst = nullptr;    // pinned staging for snapshot / apply results (read by the host)
+  size_t hst_bytes = 0;
   int64_t online_used = 0;   // memory.hpp:97 aggregate (host scalar)
   int* d_ids = nullptr;      // apply ids upload
   int64_t* d_in64 = nullptr; // cost upload
@@ -218,12 +220,29 @@ struct valve_pool {
     }
   }
 
+  // Single-CTA bookkeeping op: the kernel ends in publish(), which stores this launch's
+  // sequence number into the pinned mirror; the host polls it (wait_seq) instead of a stream
+  // synchronize.  `d` (passed by value) carries the sequence.
   template <class K, class... Args>
   void launch1(const char* op, K kernel, size_t smem, Args... args) {
     ck(cudaSetDevice(cfg.device), "cudaSetDevice");
     kernel<<<1, kNT, smem, stream>>>(args...);
     counted();
-    sync_and_check(op);
+    ck(cudaGetLastError(), op);
+    wait_seq(d.seq, op);
+  }
+  // next launch's sequence (call before building the kernel arguments from `d`)
+  void next_seq() { d.seq = ++op_seq; }
+
+  // pinned staging of `bytes` (grown on demand; the pool stream is idle when this is called)
+  uint8_t* stage(size_t bytes) {
+    if (bytes > hst_bytes) {
+      if (hst) cudaFreeHost(hst);
+      hst = nullptr;
+      hst_bytes = std::max(bytes, 2 * hst_bytes);
+      ck(cudaHostAlloc((void**)&hst, hst_bytes, cudaHostAllocDefault), "cudaHostAlloc staging");
+    }
+    return hst;
   }
 
   void counts(int64_t out[5]) const {
@@ -246,6 +265,7 @@ struct valve_pool {
     for (void* p : dev_allocs) cudaFree(p);
     if (d.pages) cudaFree(d.pages);
     if (mirror) cudaFreeHost(mirror);
+    if (hst) cudaFreeHost(hst);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev_report) cudaEventDestroy(ev_report);
@@ -550,17 +570,51 @@ void grow_tables(valve_pool* p, int R2, int P2) {
   p->cfg.max_pages_per_request = P2;
 }
 
+// The last report, staged through the pool's pinned buffer (one synchronize, DMA into pinned
+// memory), then copied into the caller's arrays.  Returns the staged arrays.
+struct Staged {
+  const int* handles;
+  const int64_t* evicted;
+  const int* inv_off;
+  const int64_t* pages;
+  const int* phys;
+  const int* blk;
+};
+
+Staged stage_apply_results(valve_pool* p, bool phys_blk) {
+  const int nh = p->last_n_handles, ne = p->last_n_evicted, np = p->last_n_pages;
+  const size_t o_ev = 0, o_pg = o_ev + (size_t)ne * 8, o_h = o_pg + (size_t)np * 8,
+               o_off = o_h + (size_t)nh * 4, o_ph = o_off + (size_t)(ne + 1) * 4,
+               o_bl = o_ph + (phys_blk ? (size_t)np * 4 : 0), total = o_bl + (phys_blk ? (size_t)np * 4 : 0);
+  uint8_t* h = p->stage(total + 16);
+  const cudaMemcpyKind k = cudaMemcpyDeviceToHost;
+  if (ne) ck(cudaMemcpyAsync(h + o_ev, p->d.res_evicted, (size_t)ne * 8, k, p->stream), "stage");
+  if (np) ck(cudaMemcpyAsync(h + o_pg, p->d.res_pages, (size_t)np * 8, k, p->stream), "stage");
+  if (nh) ck(cudaMemcpyAsync(h + o_h, p->d.res_handles, (size_t)nh * 4, k, p->stream), "stage");
+  ck(cudaMemcpyAsync(h + o_off, p->d.res_inv_off, (size_t)(ne + 1) * 4, k, p->stream), "stage");
+  if (phys_blk && np) {
+    ck(cudaMemcpyAsync(h + o_ph, p->d.res_phys, (size_t)np * 4, k, p->stream), "stage");
+    ck(cudaMemcpyAsync(h + o_bl, p->d.res_blk, (size_t)np * 4, k, p->stream), "stage");
+  }
+  ck(cudaStreamSynchronize(p->stream), "apply results");
+  return Staged{reinterpret_cast<const int*>(h + o_h), reinterpret_cast<const int64_t*>(h + o_ev),
+                reinterpret_cast<const int*>(h + o_off), reinterpret_cast<const int64_t*>(h + o_pg),
+                phys_blk ? reinterpret_cast<const int*>(h + o_ph) : nullptr,
+                phys_blk ? reinterpret_cast<const int*>(h + o_bl) : nullptr};
+}
+
 void read_apply_results(valve_pool* p, int* handles, int64_t* evicted, int* inv_off, int64_t* pages,
                         int* phys, int* blk, int cap_h, int cap_ev, int cap_pages) {
   const int nh = p->last_n_handles, ne = p->last_n_evicted, np = p->last_n_pages;
-  if (handles) p->d2h(handles, p->d.res_handles, (size_t)std::min(nh, cap_h) * 4);
-  if (evicted) p->d2h(evicted, p->d.res_evicted, (size_t)std::min(ne, cap_ev) * 8);
-  if (inv_off && cap_ev >= ne) p->d2h(inv_off, p->d.res_inv_off, (size_t)(ne + 1) * 4);
+  if (!handles && !evicted && !inv_off && !pages && !phys && !blk) return;
+  const Staged st = stage_apply_results(p, phys || blk);
+  if (handles) std::memcpy(handles, st.handles, (size_t)std::min(nh, cap_h) * 4);
+  if (evicted) std::memcpy(evicted, st.evicted, (size_t)std::min(ne, cap_ev) * 8);
+  if (inv_off && cap_ev >= ne) std::memcpy(inv_off, st.inv_off, (size_t)(ne + 1) * 4);
   const size_t n = (size_t)std::min(np, cap_pages);
-  if (pages) p->d2h(pages, p->d.res_pages, n * 8);
-  if (phys) p->d2h(phys, p->d.res_phys, n * 4);
-  if (blk) p->d2h(blk, p->d.res_blk, n * 4);
-  ck(cudaStreamSynchronize(p->stream), "apply results");
+  if (pages) std::memcpy(pages, st.pages, n * 8);
+  if (phys) std::memcpy(phys, st.phys, n * 4);
+  if (blk) std::memcpy(blk, st.blk, n * 4);
 }
 
 }  // namespace
@@ -648,14 +702,14 @@ int64_t valve_pool_quarantine_page_id(const valve_pool* p) { return (int64_t)p->
 int valve_pool_online_grow(valve_pool* p, int k, int64_t t) {
   return guard([&] {
     if (k < 0) fail(VALVE_INVALID_ARGUMENT, "online_grow: k must be >= 0");  // memory.cpp:32
-    p->launch1("online_grow", k_online_grow, 0, p->d, k, t);
+    p->next_seq(), p->launch1("online_grow", k_online_grow, 0, p->d, k, t);
   });
 }
 
 int valve_pool_online_release(valve_pool* p, int k, int* released) {
   return guard([&] {
     if (k < 0) fail(VALVE_INVALID_ARGUMENT, "online_release: k must be >= 0");  // memory.cpp:38
-    p->launch1("online_release", k_online_release, 0, p->d, k, p->online_used);
+    p->next_seq(), p->launch1("online_release", k_online_release, 0, p->d, k, p->online_used);
     *released = (int)p->mirror->r[0];
   });
 }
@@ -689,7 +743,7 @@ int valve_pool_offline_reserve(valve_pool* p, int64_t req, int pages, int64_t t,
     const int64_t HS = (int64_t)p->H * p->S;
     for (int attempt = 0;; ++attempt) {
       try {
-        p->launch1("offline_reserve", k_offline_reserve, 0, p->d, req, pages, t, max_off);
+        p->next_seq(), p->launch1("offline_reserve", k_offline_reserve, 0, p->d, req, pages, t, max_off);
         break;
       } catch (const Err&) {
         const int det = p->mirror->err_detail;
@@ -707,14 +761,14 @@ int valve_pool_offline_reserve(valve_pool* p, int64_t req, int pages, int64_t t,
 }
 
 int valve_pool_offline_release(valve_pool* p, int64_t req) {
-  return guard([&] { p->launch1("offline_release", k_offline_release, 0, p->d, req); });
+  return guard([&] { p->next_seq(), p->launch1("offline_release", k_offline_release, 0, p->d, req); });
 }
 
 int valve_pool_requests_on_handle(const valve_pool* cp, int h, int64_t* out, int cap, int* n) {
   auto* p = const_cast<valve_pool*>(cp);
   return guard([&] {
     if (h < 0 || h >= p->H) fail(VALVE_OUT_OF_RANGE, "requests_on_handle: handle out of range");
-    p->launch1("requests_on_handle", k_requests_on_handle, 0, p->d, h, (int64_t*)p->d.res_pages);
+    p->next_seq(), p->launch1("requests_on_handle", k_requests_on_handle, 0, p->d, h, (int64_t*)p->d.res_pages);
     *n = (int)p->mirror->r[0];
     if (out) p->d2h(out, p->d.res_pages, (size_t)std::min(*n, cap) * 8);
     ck(cudaStreamSynchronize(p->stream), "requests_on_handle");
@@ -724,7 +778,7 @@ int valve_pool_requests_on_handle(const valve_pool* cp, int h, int64_t* out, int
 int valve_pool_handles_of_request(const valve_pool* cp, int64_t req, int* out, int cap, int* n) {
   auto* p = const_cast<valve_pool*>(cp);
   return guard([&] {
-    p->launch1("handles_of_request", k_handles_of_request, 0, p->d, req, p->d.res_handles);
+    p->next_seq(), p->launch1("handles_of_request", k_handles_of_request, 0, p->d, req, p->d.res_handles);
     *n = (int)p->mirror->r[0];
     if (out) p->d2h(out, p->d.res_handles, (size_t)std::min(*n, cap) * 4);
     ck(cudaStreamSynchronize(p->stream), "handles_of_request");
@@ -757,29 +811,77 @@ int valve_pool_block_table(const valve_pool* cp, int64_t req, int* out, int cap,
   auto* p = const_cast<valve_pool*>(cp);
   return guard([&] {
     p->order_after_copy_plan();  // the page list is written into the report buffer
-    p->launch1("block_table", k_block_table, 0, p->d, req, p->d.res_phys);
+    p->next_seq(), p->launch1("block_table", k_block_table, 0, p->d, req, p->d.res_phys);
     *n = (int)p->mirror->r[0];
     if (out) p->d2h(out, p->d.res_phys, (size_t)std::min(*n, cap) * 4);
     ck(cudaStreamSynchronize(p->stream), "block_table");
   });
 }
 
+namespace {
+void snapshot_staged(valve_pool* p, const int** ids, const int64_t** mapped, const int** off,
+                     const int64_t** reqs, int* nh, int* nr) {
+  ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
+  k_snapshot_handles<<<(p->H + 7) / 8, 256, 0, p->stream>>>(p->d);
+  counted();
+  p->next_seq(), p->launch1("snapshot", k_snapshot, p->smem_snapshot, p->d);
+  const int h = (int)p->mirror->r[0], r = (int)p->mirror->r[1];
+  const size_t o_r = 0, o_m = o_r + (size_t)r * 8, o_i = o_m + (size_t)h * 8, o_o = o_i + (size_t)h * 4,
+               total = o_o + (size_t)(h + 1) * 4;
+  uint8_t* s = p->stage(total + 16);
+  const cudaMemcpyKind k = cudaMemcpyDeviceToHost;
+  if (r) ck(cudaMemcpyAsync(s + o_r, p->d.res_pages, (size_t)r * 8, k, p->stream), "stage");
+  if (h) ck(cudaMemcpyAsync(s + o_m, p->d.s_hmap, (size_t)h * 8, k, p->stream), "stage");
+  if (h) ck(cudaMemcpyAsync(s + o_i, p->d.s_hid, (size_t)h * 4, k, p->stream), "stage");
+  ck(cudaMemcpyAsync(s + o_o, p->d.s_roff, (size_t)(h + 1) * 4, k, p->stream), "stage");
+  ck(cudaStreamSynchronize(p->stream), "snapshot");
+  *nh = h;
+  *nr = r;
+  *reqs = reinterpret_cast<const int64_t*>(s + o_r);
+  *mapped = reinterpret_cast<const int64_t*>(s + o_m);
+  *ids = reinterpret_cast<const int*>(s + o_i);
+  *off = reinterpret_cast<const int*>(s + o_o);
+}
+}  // namespace
+
 int valve_pool_snapshot(const valve_pool* cp, int* ids, int64_t* mapped, int* off, int64_t* reqs,
                         int cap_h, int cap_r, int* nh, int* nr) {
   auto* p = const_cast<valve_pool*>(cp);
   return guard([&] {
-    ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
-    k_snapshot_handles<<<(p->H + 7) / 8, 256, 0, p->stream>>>(p->d);
-    counted();
-    p->launch1("snapshot", k_snapshot, p->smem_snapshot, p->d);
-    *nh = (int)p->mirror->r[0];
-    *nr = (int)p->mirror->r[1];
-    if (ids) p->d2h(ids, p->d.s_hid, (size_t)std::min(*nh, cap_h) * 4);
-    if (mapped) p->d2h(mapped, p->d.s_hmap, (size_t)std::min(*nh, cap_h) * 8);
-    if (off && cap_h >= *nh) p->d2h(off, p->d.s_roff, (size_t)(*nh + 1) * 4);
-    if (reqs) p->d2h(reqs, p->d.res_pages, (size_t)std::min(*nr, cap_r) * 8);
-    ck(cudaStreamSynchronize(p->stream), "snapshot");
+    const int *si, *so;
+    const int64_t *sm, *sr;
+    snapshot_staged(p, &si, &sm, &so, &sr, nh, nr);
+    if (ids) std::memcpy(ids, si, (size_t)std::min(*nh, cap_h) * 4);
+    if (mapped) std::memcpy(mapped, sm, (size_t)std::min(*nh, cap_h) * 8);
+    if (off && cap_h >= *nh) std::memcpy(off, so, (size_t)(*nh + 1) * 4);
+    if (reqs) std::memcpy(reqs, sr, (size_t)std::min(*nr, cap_r) * 8);
   });
+}
+
+int valve_pool_snapshot_view(valve_pool* p, const int** ids, const int64_t** mapped, const int** off,
+                             const int64_t** reqs, int* nh, int* nr) {
+  return guard([&] { snapshot_staged(p, ids, mapped, off, reqs, nh, nr); });
+}
+
+int valve_pool_apply_reclaim_view(valve_pool* p, const int* ids, int k, int64_t t, const int** handles,
+                                  int* n_handles, const int64_t** evicted, int* n_evicted, const int** inv_off,
+                                  const int64_t** inv_pages, int* n_pages) {
+  const int code = valve_pool_apply_reclaim(p, ids, k, t, nullptr, n_handles, nullptr, n_evicted, nullptr,
+                                            nullptr, nullptr, nullptr, 0, 0, n_pages);
+  if (code != VALVE_OK && code != VALVE_LOGIC_ERROR && code != VALVE_OUT_OF_RANGE) return code;
+  const std::string saved = g_err;
+  const int rc = guard([&] {
+    const Staged st = stage_apply_results(p, false);
+    *handles = st.handles;
+    *evicted = st.evicted;
+    *inv_off = st.inv_off;
+    *inv_pages = st.pages;
+  });
+  if (code != VALVE_OK) {
+    g_err = saved;
+    return code;
+  }
+  return rc;
 }
 
 int valve_pool_apply_reclaim(valve_pool* p, const int* ids, int k, int64_t t, int* handles,
@@ -795,7 +897,7 @@ int valve_pool_apply_reclaim(valve_pool* p, const int* ids, int k, int64_t t, in
     if (k) ck(cudaMemcpyAsync(p->d_ids, ids, (size_t)k * 4, cudaMemcpyHostToDevice, p->stream), "upload ids");
     try {
       p->order_after_copy_plan();
-      p->launch1("apply_reclaim", k_apply, p->smem_reclaim, p->d, (const int*)p->d_ids, k, t);
+      p->next_seq(), p->launch1("apply_reclaim", k_apply, p->smem_reclaim, p->d, (const int*)p->d_ids, k, t);
     } catch (const Err&) {
       p->last_n_handles = (int)p->mirror->r[0];
       p->last_n_evicted = (int)p->mirror->r[1];
@@ -848,7 +950,7 @@ int valve_pool_handle_mapped_at(const valve_pool* cp, int h, int64_t* t) {
 
 int valve_pool_check_invariants(const valve_pool* cp) {
   auto* p = const_cast<valve_pool*>(cp);
-  return guard([&] { p->launch1("check_invariants", k_check_invariants, 0, p->d, p->online_used); });
+  return guard([&] { p->next_seq(), p->launch1("check_invariants", k_check_invariants, 0, p->d, p->online_used); });
 }
 
 int valve_pool_set_costs(valve_pool* p, int n, const int64_t* reqs, const int64_t* costs) {
@@ -858,7 +960,7 @@ int valve_pool_set_costs(valve_pool* p, int n, const int64_t* reqs, const int64_
     ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
     ck(cudaMemcpyAsync(p->d_in64, reqs, (size_t)n * 8, cudaMemcpyHostToDevice, p->stream), "upload");
     ck(cudaMemcpyAsync(p->d_in64b, costs, (size_t)n * 8, cudaMemcpyHostToDevice, p->stream), "upload");
-    p->launch1("set_costs", k_set_costs, 0, p->d, n, (const int64_t*)p->d_in64,
+    p->next_seq(), p->launch1("set_costs", k_set_costs, 0, p->d, n, (const int64_t*)p->d_in64,
                (const int64_t*)p->d_in64b, 0);
     if (p->mirror->r[0]) fail(VALVE_INVALID_ARGUMENT, "set_costs: request has no live pages in the pool");
   });
@@ -874,7 +976,7 @@ int valve_pool_set_page_bytes(valve_pool* p, int n, const int64_t* reqs, const i
     ck(cudaSetDevice(p->cfg.device), "cudaSetDevice");
     ck(cudaMemcpyAsync(p->d_in64, reqs, (size_t)n * 8, cudaMemcpyHostToDevice, p->stream), "upload");
     ck(cudaMemcpyAsync(p->d_in64b, bytes, (size_t)n * 8, cudaMemcpyHostToDevice, p->stream), "upload");
-    p->launch1("set_page_bytes", k_set_costs, 0, p->d, n, (const int64_t*)p->d_in64,
+    p->next_seq(), p->launch1("set_page_bytes", k_set_costs, 0, p->d, n, (const int64_t*)p->d_in64,
                (const int64_t*)p->d_in64b, 1);
     if (p->mirror->r[0]) fail(VALVE_INVALID_ARGUMENT, "set_page_bytes: request has no live pages in the pool");
   });
@@ -903,7 +1005,8 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
     // one launch: ceil(H / 32) CTAs build the instance rows (warp per handle), the last CTA to
     // finish runs selection + apply; the host spins on the completion sequence the kernel writes
     // into the pinned mirror instead of a stream synchronize
-    const int64_t seq = ++p->op_seq;
+    p->next_seq();
+    const int64_t seq = p->d.seq;
     k_reclaim_fused<<<(p->H + 31) / 32, kNT, p->smem_reclaim, p->stream>>>(p->d, k, mode, t, seq);
     counted();
     ck(cudaGetLastError(), "reclaim");

@@ -1064,7 +1064,10 @@ def main():
         torch.cuda.set_device(gpu)
         # rank r on cuda:r; a box with fewer GPUs than ranks (functional runs only) cannot run
         # NCCL with two ranks on one device, so it falls back to gloo for the plumbing
-        dist.init_process_group("gloo" if shared else "nccl")
+        import datetime
+
+        # a hung collective aborts the job after 10 minutes instead of holding the box
+        dist.init_process_group("gloo" if shared else "nccl", timeout=datetime.timedelta(seconds=600))
         if shared and rank == 0:
             print("bench: fewer GPUs than ranks -- ranks share devices; no number here is a multi-GPU number",
                   file=sys.stderr, flush=True)

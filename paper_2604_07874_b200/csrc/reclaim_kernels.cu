@@ -353,25 +353,46 @@ __device__ void greedy_cta(int n, const int* hid, Refs R, const int* rref, const
 // on-chip.  Larger instances run CTA-wide over global scratch.
 __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, int m,
                               const int64_t* cost, int k, int64_t* marg_g, int* taken_g, int* ev,
-                              int* qoff, int* qcnt, int* qh, int* out, unsigned char* smem) {
+                              int* qoff, int* qcnt, int* qh, int* out, unsigned char* smem,
+                              int* dense = nullptr) {
   int nnz_local = 0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) nnz_local += R.end(i) - R.begin(i);
   const int nnz = block_sum(nnz_local);
   if (n <= kSmemHandles && nnz <= kSmemListings) {
-    // dense request index over the referenced requests (qcnt: flag -> dense id)
-    for (int r = threadIdx.x; r < m; r += blockDim.x) qcnt[r] = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x)
-      for (int e = R.begin(i); e < R.end(i); ++e) qcnt[rref[e]] = 1;
-    __syncthreads();
     int m2 = 0;
-    for (int base = 0; base < m; base += blockDim.x) {
-      const int r = base + threadIdx.x;
-      const int f = r < m ? qcnt[r] : 0;
-      int tot;
-      const int ex = block_excl_scan(f, tot);
-      if (r < m) qcnt[r] = f ? m2 + ex : -1;
-      m2 += tot;
+    if (dense) {
+      // dense request index: the first listing of each referenced row claims the next id
+      // (`dense` is -1 everywhere between calls; the ids are reset below through qoff)
+      __shared__ int s_m2;
+      if (threadIdx.x == 0) s_m2 = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        for (int e = R.begin(i); e < R.end(i); ++e) {
+          const int r = rref[e];
+          if (atomicCAS(&dense[r], -1, -2) == -1) {
+            const int d = atomicAdd(&s_m2, 1);
+            dense[r] = d;
+            qoff[d] = r;  // dense id -> row, for the reset
+          }
+        }
+      __syncthreads();
+      m2 = s_m2;
+      qcnt = dense;
+    } else {
+      // dense request index over the referenced requests (qcnt: flag -> dense id)
+      for (int r = threadIdx.x; r < m; r += blockDim.x) qcnt[r] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        for (int e = R.begin(i); e < R.end(i); ++e) qcnt[rref[e]] = 1;
+      __syncthreads();
+      for (int base = 0; base < m; base += blockDim.x) {
+        const int r = base + threadIdx.x;
+        const int f = r < m ? qcnt[r] : 0;
+        int tot;
+        const int ex = block_excl_scan(f, tot);
+        if (r < m) qcnt[r] = f ? m2 + ex : -1;
+        m2 += tot;
+      }
     }
     // shared-memory carve-up
     int64_t* marg = reinterpret_cast<int64_t*>(smem);
@@ -466,6 +487,8 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
       if (packed) greedy_block_packed(n, hid, Rs, rr, cost2, k, marg, skey, ev2, qoff2, qh2, out, idbits, qmax);
       else greedy_block(n, hid, Rs, rr, cost2, k, marg, ev2, qoff2, qh2, out);
     }
+    if (dense)
+      for (int d = threadIdx.x; d < m2; d += blockDim.x) dense[qoff[d]] = -1;  // back to all -1
     __syncthreads();
   } else {
     build_instance_index(n, R, rref, m, cost, marg_g, qoff, qcnt, qh, ev);
@@ -1117,7 +1140,7 @@ __device__ void reclaim_body(const PoolDev& P, int k, int mode, int64_t t, unsig
     fifo_core(n, P.s_hid, P.s_hmap, k, P.s_pick);
   } else {
     greedy_select(n, P.s_hid, R, P.s_rref, P.R, P.row_cost, k, P.s_marg, P.s_taken, P.s_ev,
-                  P.s_qoff, P.s_qcnt, P.s_qh, P.s_pick, smem);  // leaves s_ev zeroed
+                  P.s_qoff, P.s_qcnt, P.s_qh, P.s_pick, smem, P.s_dense);  // leaves s_ev zeroed
   }
   __syncthreads();
   if (threadIdx.x == 0) P.mirror->r[5] = (int64_t)globaltimer_ns();

@@ -110,6 +110,7 @@ struct PoolDev {
   uint64_t* s_key;   // [pow2(H*S)]
   int* s_pay;        // [pow2(H*S)]
   int* s_cnt;        // [H]
+  int* s_dense;      // [R] row -> dense request index during a greedy re-index; -1 between calls
   int64_t seq;       // this launch's completion sequence (publish() stores it into the mirror)
   unsigned* ticket;  // [1] CTAs of the fused reclaim's instance pass that finished (last one goes on)
   int* s_tphys;      // [H*S] apply tuples: physical page

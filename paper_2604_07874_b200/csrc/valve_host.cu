@@ -357,6 +357,8 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
   d.s_rref = p->dalloc<int>(HS);
   d.s_qoff = p->dalloc<int>(R + 1);
   d.s_qcnt = p->dalloc<int>(HSR);
+  d.s_dense = p->dalloc<int>(R);
+  ck(cudaMemset(d.s_dense, 0xff, (size_t)R * 4), "memset");
   d.s_qh = p->dalloc<int>(HS);
   d.s_marg = p->dalloc<int64_t>(H);
   d.s_taken = p->dalloc<int>(H);
@@ -522,6 +524,7 @@ void grow_tables(valve_pool* p, int R2, int P2) {
     regrow(p, d.s_ev, 0, R2, 0);
     regrow(p, d.s_qoff, 0, R2 + 1, -1);
     regrow(p, d.s_qcnt, 0, std::max<int64_t>(HS, R2), -1);
+    regrow(p, d.s_dense, 0, R2, -1);
     regrow(p, d.s_evrows, 0, R2, -1);
     regrow(p, d.s_rank, 0, R2, -1);
     regrow(p, d.res_evicted, R, R2, 0);
@@ -1819,11 +1822,12 @@ int valve_gate_release(valve_gate* g, uint32_t gen, void* s) {
     ck(cudaSetDevice(g->device), "cudaSetDevice");
     std::vector<valve_gate*> all{g};
     all.insert(all.end(), g->peers.begin(), g->peers.end());
-    // reopen every member first (offline work resumes after N memops, not 3N), then clear the
-    // diagnostics for the next raise (same stream: done before it) and stamp the leader's gen
+    // clear the diagnostics first (nothing polls a closed gate, and a raise issued on another
+    // stream after this release cannot have its first-seen stamp wiped), then reopen every
+    // member and stamp the leader's gen
     MemBatch b;
-    for (valve_gate* x : all) b.write32(&x->d->closed, 0);
     for (valve_gate* x : all) b.write64(&x->d->t_first_seen, 0);
+    for (valve_gate* x : all) b.write32(&x->d->closed, 0);
     b.write32(&g->d->gen, gen);
     b.submit(op, st);
   });

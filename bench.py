@@ -811,7 +811,7 @@ def run_valve(args, rank, world, dist):
             policies=tuple(p for p in args.rt_policies.split(",") if p),
             log_dir=os.path.join(ROOT, "gpurun_out", "realtime_logs")))
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "r1_copy_traffic.json")))
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r2_copy_traffic.json")))
     except OSError:
         traffic = {}
     value = total_bytes / (elapsed_ms * 1e-3) / 1e9

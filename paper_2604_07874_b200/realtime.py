@@ -606,6 +606,7 @@ class RunResult:
     prefill_us: List[float] = field(default_factory=list)
     step_gap_us: List[float] = field(default_factory=list)  # host time between back-to-back busy steps
     decode_gpu_us: List[float] = field(default_factory=list)  # device time of each decode graph replay
+    slow_iterations: List[dict] = field(default_factory=list)  # loop iterations with > 3 ms host time
     log: EventLog = field(default_factory=EventLog)
     plan: list = field(default_factory=list)
 
@@ -1090,14 +1091,29 @@ class Colocation:
         self._t0 = t0
         now_us = lambda: int((time.perf_counter() - t0) * 1e6)  # noqa: E731
         stop_us = int((horizon_s + tail_s) * 1e6)
+        pc = time.perf_counter
+        marks = []  # (phase, perf_counter) of the current loop iteration, for the slow-iteration log
+
+        def slow_check(where):
+            # an iteration that spent > 3 ms of host time before its step (or before going idle)
+            if marks and pc() - marks[0][1] > 3e-3:
+                self.res.slow_iterations.append(
+                    {"t_us": int((marks[0][1] - t0) * 1e6), "where": where,
+                     "phases_us": {marks[i][0]: int((marks[i][1] - marks[i - 1][1]) * 1e6) for i in range(1, len(marks))},
+                     "total_us": int((pc() - marks[0][1]) * 1e6)})
+
         while True:
+            marks.clear()
+            marks.append(("top", pc()))
             now = now_us()
             if now > stop_us:
                 break
             if self.colocated:
                 self._fire_timers(now)
+                marks.append(("timers", pc()))
                 if not busy:  # gated while busy: nothing to harvest
                     self._harvest(now)
+                    marks.append(("harvest", pc()))
             while nxt < len(reqs) and reqs[nxt].arrival_us <= now:
                 r = reqs[nxt]
                 log.add(r.arrival_us, "arrival", **{"class": "online"}, request_id=r.rid, gpu=0,
@@ -1153,10 +1169,13 @@ class Colocation:
                         self.offline.admit(now)
                 if finished and not stalled:
                     break
+                marks.append(("idle_edge", pc()))
                 if self.colocated and self._offline_allowed():
                     self._launch_offline()
                     if stalled:
                         self.offline.admit(now)
+                marks.append(("launch_offline", pc()))
+                slow_check("idle")
                 time.sleep(50e-6)
                 continue
             stalled = False
@@ -1181,15 +1200,20 @@ class Colocation:
                     e1.record(self.online)
                     pending_wait = (e0, e1)
                     self.res.disables = self.channel.disables_issued()
+                marks.append(("busy_edge", pc()))
             if act[0] == "prefill":
                 r = by_rid[act[1]]
                 queue.remove(r)
                 self._acquire(need, now)
+                marks.append(("acquire", pc()))
                 r.pages = self.pages.alloc(need, r.rid)
+                marks.append(("alloc", pc()))
                 if pending_wait is not None:
                     wait_events.append((now, r.rid, pending_wait))
                     pending_wait = None
                 toks = torch.randint(0, m.s.vocab, (r.prompt,), device=self.dev)
+                marks.append(("tokens", pc()))
+                slow_check("prefill")
                 t_it = now_us()
                 if gap_from is not None:
                     self.res.step_gap_us.append(t_it - gap_from)
@@ -1207,6 +1231,7 @@ class Colocation:
             # one decode iteration over the batch
             if need:
                 self._acquire(need, now)
+                marks.append(("acquire", pc()))
             new_slots = []
             for r, nb in zip(decoding, need_by):
                 if nb:
@@ -1217,6 +1242,8 @@ class Colocation:
                 tgt = self.pages.full_target(new_slots)
                 if tgt:
                     self.pool.wait_landed(tgt, self.online.cuda_stream)
+            marks.append(("alloc", pc()))
+            slow_check("decode")
             t_it = now_us()
             if gap_from is not None:
                 self.res.step_gap_us.append(t_it - gap_from)
@@ -1503,6 +1530,8 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
             "pressure_events": r.pressure, "stalls": r.stalls,
             "copy_gb": r.copy_bytes / 1e9, "copy_gbs_mean": (sum(r.copy_gbs) / len(r.copy_gbs)) if r.copy_gbs else None,
             "decision_us_p50": _pct([d for x in rs for d in x.decision_us], 50),
+            "slow_iterations": {"n": sum(len(x.slow_iterations) for x in rs),
+                                "worst": sorted((w for x in rs for w in x.slow_iterations), key=lambda w: -w["total_us"])[:5]},
             "decode_iter_ms_mean": sum(d for x in rs for d in x.decode_iter_us) / max(1, sum(len(x.decode_iter_us) for x in rs)) / 1e3,
             "step_gap_us_mean": sum(d for x in rs for d in x.step_gap_us) / max(1, sum(len(x.step_gap_us) for x in rs)),
             "decode_gpu_ms_mean": sum(d for x in rs for d in x.decode_gpu_us) / max(1, sum(len(x.decode_gpu_us) for x in rs)) / 1e3,
@@ -1536,6 +1565,9 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
                        "decode_gpu_ms_mean": sum(d for x in solos for d in x.decode_gpu_us) / max(1, sum(len(x.decode_gpu_us) for x in solos)) / 1e3,
                        "step_gap_us_p99": _pct([d for x in solos for d in x.step_gap_us], 99),
                        "plan_deviations": [_deviations(plan, x.plan) for x in solos],
+                       "slow_iterations": {"n": sum(len(x.slow_iterations) for x in solos),
+                                           "worst": sorted((w for x in solos for w in x.slow_iterations),
+                                                           key=lambda w: -w["total_us"])[:5]},
                        "clocks": [x.clocks for x in solos]},
         colos[0].policy: arm(colos),
         **{pol: arm([r]) for pol, r in extra.items()},

@@ -175,8 +175,9 @@ int valve_pool_reclaim_copy(valve_pool* p, void* host_dst, int64_t dst_bytes,
  * works from its own device snapshot of the report, so bookkeeping calls (reserve/release/
  * grow/...) and the NEXT apply_reclaim / reclaim proceed on the pool stream while the bytes
  * cross the link (back-to-back reclaim ops keep the link busy).  fill_pages / restore wait for
- * the copy (they rewrite page bytes).  Up to two copies in flight; each _wait completes the
+ * the copy (they rewrite page bytes).  Up to VALVE_COPY_RING copies in flight; each _wait completes the
  * oldest one (FIFO) and returns its stats.  The synchronous form requires none in flight. */
+#define VALVE_COPY_RING 8
 int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_bytes,
                                   const valve_copy_params* params);
 int valve_pool_reclaim_copy_wait(valve_pool* p, valve_copy_stats* stats);

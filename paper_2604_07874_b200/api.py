@@ -32,6 +32,7 @@ from typing import Callable, Dict, List, Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIBVALVE = os.path.join(_HERE, "libvalve.so")
+COPY_RING = 8  # VALVE_COPY_RING (valve_cuda.h): reclaim copies in flight per pool
 
 
 class LogicError(Exception):

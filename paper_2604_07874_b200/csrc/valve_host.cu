@@ -160,7 +160,7 @@ struct valve_pool {
   unsigned long long* d_landed = nullptr;  // published copy waves (monotone, all copies)
   unsigned long long* d_tat = nullptr;     // rate bound: GCRA theoretical arrival time (ns)
   uint64_t waves_issued = 0;               // sum of n_waves over started copies
-  static constexpr int kCopySlots = 2;
+  static constexpr int kCopySlots = VALVE_COPY_RING;
   CopySlot cs[kCopySlots];
   int cs_head = 0, cs_n = 0, cs_last = -1;
 
@@ -1105,7 +1105,7 @@ int valve_pool_reclaim_copy_start(valve_pool* p, void* host_dst, int64_t dst_byt
     if (c.chunk_bytes % 16 || c.threads % 32 || c.threads > 512)
       fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: chunk must be a 16-byte multiple, threads <= 512");
     if (p->cs_n == valve_pool::kCopySlots)
-      fail(VALVE_LOGIC_ERROR, "reclaim_copy: two copies already in flight (call reclaim_copy_wait)");
+      fail(VALVE_LOGIC_ERROR, "reclaim_copy: the copy ring is full (call reclaim_copy_wait)");
     const int64_t need = p->last_copy_bytes;
     if (dst_bytes < need) fail(VALVE_INVALID_ARGUMENT, "reclaim_copy: destination too small");
     if (reinterpret_cast<uintptr_t>(host_dst) % 16)

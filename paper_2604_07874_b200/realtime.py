@@ -350,7 +350,12 @@ class OnlinePages:
     The reference charges online pages as an aggregate (memory.hpp:97, sim.cpp:513-526); a real
     tenant needs the slots, so this mirrors which handles are online and which of their slots
     hold KV.  Slots whose old bytes a reclaim copy has not yet read out carry that copy's ticket
-    (valve_pool_copy_ticket): a write waits for the waves under the bytes it writes."""
+    (valve_pool_copy_ticket): a write waits for the waves under the bytes it writes.
+
+    Free slots live in two places so allocation never scans them all: `clean` (no pending
+    ticket; a max-heap, highest slot first -- releases take the lowest handle ids,
+    memory.cpp:37-51) and `pending` (ticketed, usually one op's slots).  `free` is the set of
+    both; heap entries of slots that left `free` are dropped lazily."""
 
     def __init__(self, pool: A.DevicePool, layer_bytes: int = LAYER_BYTES):
         self.pool = pool
@@ -358,47 +363,100 @@ class OnlinePages:
         self.layer_bytes = layer_bytes
         self.handles: set = set()
         self.free: set = set()
+        self.clean: list = []               # heap of -slot
+        self.pending: set = set()
         self.used: Dict[int, int] = {}      # slot -> request id
         self.ticket: Dict[int, tuple] = {}  # slot -> (wave_base, n_waves, wave_bytes)
         self.landed = 0
+
+    def _free_slot(self, s):
+        self.free.add(s)
+        if s in self.ticket:
+            self.pending.add(s)
+        else:
+            heapq.heappush(self.clean, -s)
 
     def refresh_landed(self):
         self.landed = self.pool.landed()[0]
         done = [s for s, (b, n, _) in self.ticket.items() if b + n <= self.landed]
         for s in done:
             del self.ticket[s]
+            if s in self.pending:
+                self.pending.discard(s)
+                heapq.heappush(self.clean, -s)
 
     def set_tickets(self, slots, ticket):
         for s in slots:
             self.ticket[s] = ticket
+            if s in self.free:
+                self.pending.add(s)  # its clean heap entry is skipped on pop
 
     def sync_handles(self):
         ids = set(self.pool.online_handle_ids())
         for h in ids - self.handles:
-            self.free.update(range(h * self.S, (h + 1) * self.S))
+            for s in range(h * self.S, (h + 1) * self.S):
+                self._free_slot(s)
         for h in self.handles - ids:
             for s in range(h * self.S, (h + 1) * self.S):
                 assert s not in self.used, f"online handle {h} released with live KV in slot {s}"
                 self.free.discard(s)
+                self.pending.discard(s)
         self.handles = ids
 
-    def alloc(self, n: int, rid: int) -> List[int]:
-        """n free slots: landed ones first (lowest ticket pressure), then pending by ticket, and
-        among equals the highest handles first (releases take the lowest ids, memory.cpp:37-51)."""
+    def _pop_clean(self, exclude_handles=()):
+        """Highest clean free slot (not in exclude_handles), or None."""
+        skipped = []
+        got = None
+        while self.clean:
+            s = -heapq.heappop(self.clean)
+            if s not in self.free or s in self.ticket:
+                continue  # stale entry (left the free set / got a ticket since)
+            if s // self.S in exclude_handles:
+                skipped.append(s)
+                continue
+            got = s
+            self.free.discard(s)  # taken now: a duplicate heap entry of s is stale from here on
+            break
+        for s in skipped:
+            heapq.heappush(self.clean, -s)
+        return got
+
+    def alloc(self, n: int, rid: int, exclude_handles=()) -> List[int]:
+        """n free slots: clean ones first (highest first), then pending by ticket."""
         if n > len(self.free):
             raise RuntimeError(f"online slots: need {n}, have {len(self.free)}")
         if self.ticket:
             self.refresh_landed()
-        pick = sorted(self.free, key=lambda s: (self.ticket.get(s, (-1, 0, 0))[0], -s))[:n]
+        pick = []
+        while len(pick) < n:
+            s = self._pop_clean(exclude_handles)
+            if s is None:
+                break
+            pick.append(s)
+        if len(pick) < n:
+            rest = sorted((s for s in self.pending if s // self.S not in exclude_handles),
+                          key=lambda s: (self.ticket[s][0], -s))[: n - len(pick)]
+            if len(rest) < n - len(pick):
+                for s in pick:  # not enough: give back
+                    self._free_slot(s)
+                raise RuntimeError(f"online slots: need {n}, have {len(pick) + len(rest)} outside {exclude_handles}")
+            pick += rest
         for s in pick:
             self.free.discard(s)
+            self.pending.discard(s)
             self.used[s] = rid
         return pick
+
+    def clean_count_outside(self, handles) -> int:
+        """Free slots without a pending ticket outside `handles` (O(|handles| * S))."""
+        inside = sum(1 for h in handles for s in range(h * self.S, (h + 1) * self.S)
+                     if s in self.free and s not in self.pending)
+        return len(self.free) - len(self.pending) - inside
 
     def release(self, slots):
         for s in slots:
             del self.used[s]
-            self.free.add(s)
+            self._free_slot(s)
 
     def layer_target(self, slots, li: int) -> int:
         """Landed count a write of layer li (slot bytes [li, li+1) * layer_bytes) into `slots`
@@ -502,15 +560,21 @@ class OfflineEngine:
     def costs(self):
         return {r.rid: r.recompute_cost() for r in self.running.values()}
 
-    def advance(self, forwards: float, now: int, horizon_us: int):
+    def advance(self, forwards: float, now: int, horizon_us: int, budget_s: float = 1e-3):
         """Spend harvested token-forwards, iteration by iteration as a continuous-batching engine
         does: one decode step of the running batch (one forward per request), then a prefill
-        chunk of up to `chunk` forwards of the FIFO head(s).  Returns whether pages were freed."""
+        chunk of up to `chunk` forwards of the FIFO head(s).  Returns whether pages were freed.
+        At most `budget_s` of host time per call: forwards not spent yet stay in the carry and are
+        spent by the next calls (the engine's bookkeeping must never hold the serving loop)."""
         self.forwards += forwards
-        f = int(forwards + self.carry)
-        self.carry = forwards + self.carry - f
+        total = forwards + self.carry
+        f = int(total)
+        frac = total - f
+        deadline = time.perf_counter() + budget_s
         freed = False
         while f > 0:
+            if time.perf_counter() > deadline:
+                break
             progressed = False
             batch = self.decoding[: self.max_batch]
             if batch and f >= len(batch):
@@ -546,8 +610,8 @@ class OfflineEngine:
                     r.state = "decode"
                     self.decoding.append(r.rid)
             if not progressed:
-                self.carry += f
                 break
+        self.carry = frac + f  # unspent forwards (budget reached, or nothing to run)
         return freed
 
     def on_evicted(self, rids, now: int, kill: bool):
@@ -607,6 +671,7 @@ class RunResult:
     step_gap_us: List[float] = field(default_factory=list)  # host time between back-to-back busy steps
     decode_gpu_us: List[float] = field(default_factory=list)  # device time of each decode graph replay
     slow_iterations: List[dict] = field(default_factory=list)  # loop iterations with > 3 ms host time
+    deferred_releases: int = 0  # MIAD releases postponed: no copied-out slots to move the KV into
     log: EventLog = field(default_factory=EventLog)
     plan: list = field(default_factory=list)
 
@@ -626,7 +691,7 @@ class RtConfig:
     copy_rate_gbs: float = 32.0           # rate bound of the reclaim copies (bytes per window)
     copy_burst_bytes: int = 64 << 20
     copy_ctas: int = 8
-    copy_buffer_bytes: int = 6 << 30      # pinned destination per in-flight copy
+    copy_buffer_bytes: int = 6 << 30      # largest reclaim op's bytes; the pinned arena is twice this
     static_window_frac: float = 0.1       # scenario.hpp:51
     seed: int = 2604
 
@@ -647,7 +712,7 @@ class Colocation:
     """One run of one policy on a shared pool + model (the pool is reset per run)."""
 
     def __init__(self, model: OnlineModel, pool: A.DevicePool, cfg: RtConfig, offline_backlog=(),
-                 gemm_chain=None, host_bufs=None):
+                 gemm_chain=None, host_bufs=None):  # host_bufs: the pinned copy arena (api.HostBuffer)
         self.m, self.pool, self.cfg = model, pool, cfg
         self.policy = cfg.policy
         self.colocated = cfg.policy != "standalone"
@@ -660,11 +725,17 @@ class Colocation:
         self.pool_stream = torch.cuda.ExternalStream(pool.view().stream, device=self.dev)
         self.backlog = offline_backlog
         self.gemm_chain = gemm_chain  # list of (a, b, c, m, n, k, tiles)
-        self.host_bufs = host_bufs or []
+        self.arena = host_bufs  # one pinned HostBuffer: the copies' destination ring
         self.timers: list = []
         self.seq = 0
 
     # ----------------------------------------------------------------- timers / channel
+    def _mark(self, name):
+        """Phase stamp for the slow-iteration log (no-op outside run())."""
+        m = getattr(self, "_marks", None)
+        if m is not None:
+            m.append((name, time.perf_counter()))
+
     def _schedule(self, when, kind, *args):
         heapq.heappush(self.timers, (int(when), self.seq, kind, args))
         self.seq += 1
@@ -682,6 +753,7 @@ class Colocation:
                 self._reservation_window(when)
             elif kind == "calib":
                 self._calibration_end(when)
+            self._mark("timer:" + kind)
 
     def _on_enabled(self, t):
         self._launch_offline()
@@ -742,6 +814,7 @@ class Colocation:
             return
         self._last_harvest = now
         st = self.ggate.read()
+        self._mark("harvest:gate_read")
         cur = self.gemm_chain[self._gi]
         # tiles of the completed GEMMs of the chain + the running one's (a whole pass of the chain
         # is one forward of gemm_tokens tokens)
@@ -749,8 +822,11 @@ class Colocation:
         per_token = QWEN_FLOP_PER_TOKEN * self.cfg.gemm_layers / 28
         fwd = (flop - self._flop_accounted) / per_token if flop > self._flop_accounted else 0.0
         self._flop_accounted = max(self._flop_accounted, flop)
-        if fwd > 0 and self.offline.advance(fwd, now, self.horizon_us) and not self._busy:
+        freed = fwd > 0 and self.offline.advance(fwd, now, self.horizon_us)
+        self._mark("harvest:advance")
+        if freed and not self._busy:
             self.offline.admit(now)  # while the lane is busy, admission waits for the idle edge
+            self._mark("harvest:admit")
 
     def _chain_flop_of(self, tiles_total):
         """FLOP of the first `tiles_total` tiles of the (cyclic) chain."""
@@ -877,19 +953,17 @@ class Colocation:
         t4 = time.perf_counter()
         for key, a_, b_ in (("costs", t0, t1), ("order", t1, td), ("decision", td, t3), ("result", t3, t4)):
             ph[key] = ph.get(key, 0.0) + (b_ - a_) * 1e6
+        self._mark("reclaim:decision")
         if self.cfg.copy and not kill and npg:
-            if len(self._copies) == 2:
-                self._complete_copy()
-            buf = self.host_bufs[self._next_buf % len(self.host_bufs)]
-            self._next_buf += 1
             total, _ = self.pool.last_copy_layout()
-            assert total <= buf.nbytes, "reclaim op larger than the pinned copy buffer"
-            self.pool.reclaim_copy_start(buf.ptr, buf.nbytes, A.copy_params(
+            off = self._arena_alloc(total)
+            self._mark("reclaim:arena")
+            self.pool.reclaim_copy_start(self.arena.ptr + off, total, A.copy_params(
                 ctas=self.cfg.copy_ctas, rate_bytes_per_s=self.cfg.copy_rate_gbs * 1e9,
                 burst_bytes=self.cfg.copy_burst_bytes))
             ticket = self.pool.copy_ticket()
             self.pages.set_tickets([p for r in res.evicted_requests for p in res.physical_pages[r]], ticket)
-            self._copies.append(op)
+            self._copies.append((op, off, total))
             self.res.copy_bytes += total
             if purpose == "shortfall":
                 # when could the waiting online request write its first layer (wave 0 out) and
@@ -920,6 +994,29 @@ class Colocation:
             self.res.kills += ne
         else:
             self.res.evictions += ne
+
+    def _arena_alloc(self, nbytes: int) -> int:
+        """Destination of the next copy in the pinned arena, used as a FIFO byte ring: at most
+        VALVE_COPY_RING copies in flight and no overlap with an in-flight copy's bytes; only when
+        the ring is full does the host wait (for the oldest copy) -- never per op."""
+        size = self.arena.nbytes
+        assert nbytes <= size, "reclaim op larger than the pinned copy arena"
+        while True:
+            if len(self._copies) >= A.COPY_RING:
+                self._complete_copy()
+                continue
+            if not self._copies:
+                return 0
+            head_off = self._copies[0][1]
+            tail_end = self._copies[-1][1] + self._copies[-1][2]
+            if tail_end >= head_off:  # in-flight bytes [head_off, tail_end): free tail, then wrap to 0
+                if tail_end + nbytes <= size:
+                    return tail_end
+                if nbytes <= head_off:
+                    return 0
+            elif tail_end + nbytes <= head_off:  # wrapped: free gap [tail_end, head_off)
+                return tail_end
+            self._complete_copy()
 
     def _complete_copy(self):
         self._copies.pop(0)
@@ -954,20 +1051,22 @@ class Colocation:
         going = sorted(self.pages.handles)[:r]
         move = [s for h in going for s in range(h * S, (h + 1) * S) if s in self.pages.used]
         if move:
-            keep_free = [s for s in self.pages.free if s // S not in going]
-            assert len(keep_free) >= len(move)
-            dst = sorted(keep_free, key=lambda s: (self.pages.ticket.get(s, (-1, 0, 0))[0], -s))[: len(move)]
-            tgt = self.pages.full_target(dst)
+            # move the KV out of the handles going back -- only into slots whose old bytes are
+            # already out (no ticket): a release must never make the online lane wait for a copy;
+            # if there are not enough such slots the release waits for a later tick
+            if self.pages.ticket:
+                self.pages.refresh_landed()
+            if self.pages.clean_count_outside(set(going)) < len(move):
+                self.res.deferred_releases += 1
+                return 0
+            dst = self.pages.alloc(len(move), -2, exclude_handles=set(going))
             with torch.cuda.stream(self.online):
-                if tgt:
-                    self.pool.wait_landed(tgt, self.online.cuda_stream)
-                si = torch.tensor(move, device=self.dev)
-                di = torch.tensor(dst, device=self.dev)
-                self.m.u8.index_copy_(0, di, self.m.u8.index_select(0, si))
+                # slot-to-slot device copies: no temporary (a fresh 2 MiB x n allocation can make
+                # the caching allocator call cudaMalloc, which waits for the running reclaim copies)
+                for a_, b_ in zip(move, dst):
+                    self.m.u8[b_].copy_(self.m.u8[a_])
             for s, d in zip(move, dst):
                 rid = self.pages.used.pop(s)
-                self.pages.free.add(s)
-                self.pages.free.discard(d)
                 self.pages.used[d] = rid
                 if rid < 0:
                     self._scratch = d
@@ -975,7 +1074,9 @@ class Colocation:
                     req = self._by_rid[rid]
                     req.pages[req.pages.index(s)] = d
             self.online.synchronize()
+            self._mark("release:move")
         got = P.online_release(r)
+        self._mark("release:pool")
         assert got == r, (got, r)
         self.pages.sync_handles()
         return got
@@ -1030,7 +1131,7 @@ class Colocation:
         self.pages = OnlinePages(P)
         self.offline = OfflineEngine(P, self.backlog if self.colocated else [], log)
         self.observer = torch.cuda.Stream(device=self.dev)
-        self._copies, self._next_buf, self._shortfall_marks = [], 0, []
+        self._copies, self._shortfall_marks = [], []
         self._waited_gen = -1
         self._decode_tiles = 0
         self._gi, self._gemm_done_tiles, self._flop_accounted, self._last_harvest = 0, 0, 0.0, 0
@@ -1092,14 +1193,15 @@ class Colocation:
         now_us = lambda: int((time.perf_counter() - t0) * 1e6)  # noqa: E731
         stop_us = int((horizon_s + tail_s) * 1e6)
         pc = time.perf_counter
-        marks = []  # (phase, perf_counter) of the current loop iteration, for the slow-iteration log
+        marks = self._marks = []  # (phase, perf_counter) of this loop iteration, for the slow-iteration log
 
         def slow_check(where):
             # an iteration that spent > 3 ms of host time before its step (or before going idle)
             if marks and pc() - marks[0][1] > 3e-3:
                 self.res.slow_iterations.append(
                     {"t_us": int((marks[0][1] - t0) * 1e6), "where": where,
-                     "phases_us": {marks[i][0]: int((marks[i][1] - marks[i - 1][1]) * 1e6) for i in range(1, len(marks))},
+                     "phases_us": [[marks[i][0], int((marks[i][1] - marks[i - 1][1]) * 1e6)]
+                                   for i in range(1, len(marks)) if marks[i][1] - marks[i - 1][1] > 2e-4],
                      "total_us": int((pc() - marks[0][1]) * 1e6)})
 
         while True:
@@ -1470,7 +1572,7 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
     model.bind(pool)
     trace = spike_trace(seed, horizon, base, spike, period, width, prompt=prompt, output=output)
     backlog = offline_population(seed + 1, 20 * handles)
-    bufs = [A.HostBuffer(cfg.copy_buffer_bytes) for _ in range(2)]
+    bufs = A.HostBuffer(2 * cfg.copy_buffer_bytes)
     warm(model, pool, trace)
     plan = None
     for _ in range(2):  # the second of two live standalone runs (the first pays first-use costs)
@@ -1526,7 +1628,8 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
             "offline_decode_gbs": r.offline_decode_bytes / r.wall_s / 1e9,
             "disables": r.disables, "disables_per_request": r.disables / max(1, len(trace)),
             "reclaims": r.reclaims, "reclaimed_handles": r.reclaimed_handles, "evictions": r.evictions,
-            "kills": r.kills, "releases": r.releases, "interval_changes": r.interval_changes,
+            "kills": r.kills, "releases": r.releases, "deferred_releases": r.deferred_releases,
+            "interval_changes": r.interval_changes,
             "pressure_events": r.pressure, "stalls": r.stalls,
             "copy_gb": r.copy_bytes / 1e9, "copy_gbs_mean": (sum(r.copy_gbs) / len(r.copy_gbs)) if r.copy_gbs else None,
             "decision_us_p50": _pct([d for x in rs for d in x.decision_us], 50),

@@ -226,12 +226,18 @@ def test_pipelined_copies_back_to_back_reclaims(oracle_c):
     assert n2 > 0 and set(res2.handles).isdisjoint(res1.handles)
     buf2 = A.HostBuffer(n2 * pool.page_bytes)
     pool.reclaim_copy_start(buf2.ptr, buf2.nbytes, A.copy_params(ctas=4, chunk_bytes=8192))
-    with pytest.raises(A.LogicError):  # a third copy would exceed the ring
-        pool.reclaim_copy_start(buf2.ptr, buf2.nbytes)
     with pytest.raises(A.LogicError):  # the synchronous form needs an idle ring
         pool.reclaim_copy(buf2.ptr, buf2.nbytes)
+    # the same report again until the ring (VALVE_COPY_RING slots) is full, then one more fails
+    spare = A.HostBuffer(n2 * pool.page_bytes)
+    for _ in range(A.COPY_RING - 2):
+        pool.reclaim_copy_start(spare.ptr, spare.nbytes, A.copy_params(ctas=4, chunk_bytes=8192))
+    with pytest.raises(A.LogicError):
+        pool.reclaim_copy_start(spare.ptr, spare.nbytes)
     st1 = pool.reclaim_copy_wait()
     st2 = pool.reclaim_copy_wait()
+    for _ in range(A.COPY_RING - 2):
+        assert pool.reclaim_copy_wait().bytes == n2 * pool.page_bytes
     assert (st1.bytes, st2.bytes) == (n1 * pool.page_bytes, n2 * pool.page_bytes)
     assert np.array_equal(buf1.view(), _expected_images(oracle_c, res1, pool.page_bytes))
     assert np.array_equal(buf2.view(), _expected_images(oracle_c, res2, pool.page_bytes))

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -623,6 +624,15 @@ void read_apply_results(valve_pool* p, int* handles, int64_t* evicted, int* inv_
 }
 
 }  // namespace
+
+// The colocation runtime keeps many streams busy at once (online, offline tenant, gate, pool, copy,
+// plan, observers) and some of them block on stream memory operations for long periods (a gated
+// launch waits for the gate to open; a landed-ticket wait lasts until its copy wave is out).  With
+// CUDA's default of 8 hardware work queues, streams share queues and a blocked wait stalls every
+// stream behind it in the same queue (measured: a 1-CTA pool op delayed 90 ms behind a ticket
+// wait).  Ask for the maximum number of queues before the process creates its CUDA context; a
+// caller's own setting wins.
+__attribute__((constructor)) static void valve_connections() { setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0); }
 
 extern "C" {
 

@@ -522,6 +522,7 @@ class OfflineEngine:
         self.lost = 0         # forwards thrown away by evictions / kills
         self.tokens_done = 0  # generated tokens of completed requests (metrics.cpp offline_tokens)
         self.completed = 0
+        self.mark = lambda name: None  # phase stamps for the serving loop's slow-iteration log
 
     def pages(self, r: OffReq) -> int:
         return -(-(r.input + r.output) // self.page_tokens)
@@ -588,7 +589,9 @@ class OfflineEngine:
                         r.state = "done"
                         self.decoding.remove(rid)
                         del self.running[rid]
+                        self.mark("advance:loop")
                         self.pool.offline_release(rid)
+                        self.mark("advance:release")
                         freed = True
                         if now <= horizon_us:
                             self.tokens_done += r.generated
@@ -1130,6 +1133,7 @@ class Colocation:
         P.reset()
         self.pages = OnlinePages(P)
         self.offline = OfflineEngine(P, self.backlog if self.colocated else [], log)
+        self.offline.mark = self._mark
         self.observer = torch.cuda.Stream(device=self.dev)
         self._copies, self._shortfall_marks = [], []
         self._waited_gen = -1

@@ -111,9 +111,28 @@ __global__ void k_paged_combine(const float* __restrict__ part_acc, const float*
   out[((int64_t)b * hq + h) * kD + d] = __float2bfloat16(den > 0.f ? num / den : 0.f);
 }
 
+// SM clock probe (diagnostics of the real-time harness): one thread spins ~4 us of %globaltimer
+// and stores the SM clock (clock64 ticks per ns * 1000 = MHz) into out[slot].
+__global__ void k_clock_probe(float* out, int slot) {
+  uint64_t g0, g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  const long long c0 = clock64();
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  } while (g1 - g0 < 4000);
+  const long long c1 = clock64();
+  out[slot] = (float)(c1 - c0) * 1000.f / (float)(g1 - g0);
+}
+
 }  // namespace
 
 extern "C" {
+
+int online_clock_probe(float* out, int slot, void* stream) {
+  k_clock_probe<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(out, slot);
+  return (int)cudaGetLastError();
+}
+
 
 // q, out: bf16 [B, hq, 128] (device).  bt: int32 [B, bt_stride] physical slots, lens: int32 [B]
 // tokens to attend (incl. the one just written).  part_acc: fp32 [B*hq*splits*128], part_ml:

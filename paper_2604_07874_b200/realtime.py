@@ -98,6 +98,10 @@ class OnlineModel:
         self.lm = w(s.d, s.vocab)
         self.device = device
         self.lib = C.CDLL(LIBONLINE)
+        self.lib.online_clock_probe.restype = C.c_int
+        self.lib.online_clock_probe.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        self.clock_mhz = torch.zeros(1 << 16, dtype=torch.float32, device=device)  # per decode step
+        self.clock_n = 0
         self.lib.online_paged_decode_attn.restype = C.c_int
         self.lib.online_paged_decode_attn.argtypes = [
             C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int, C.c_void_p,
@@ -253,6 +257,11 @@ class OnlineModel:
             self.s_len[:B] = d[:, 3].to(torch.int32)
             self.s_bt[:B] = d[:, 4:].to(torch.int32)
             g = self._graph(B)
+            if self.gpu_events is not None and self.clock_n < self.clock_mhz.numel():
+                # SM clock at the start of the step (a 4 us probe kernel on the online stream)
+                self.lib.online_clock_probe(C.c_void_p(self.clock_mhz.data_ptr()), self.clock_n,
+                                            C.c_void_p(torch.cuda.current_stream().cuda_stream))
+                self.clock_n += 1
             if self.gpu_events is not None:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
@@ -673,6 +682,7 @@ class RunResult:
     prefill_us: List[float] = field(default_factory=list)
     step_gap_us: List[float] = field(default_factory=list)  # host time between back-to-back busy steps
     decode_gpu_us: List[float] = field(default_factory=list)  # device time of each decode graph replay
+    decode_sm_mhz: List[float] = field(default_factory=list)  # SM clock at the start of each replay
     slow_iterations: List[dict] = field(default_factory=list)  # loop iterations with > 3 ms host time
     deferred_releases: int = 0  # MIAD releases postponed: no copied-out slots to move the KV into
     log: EventLog = field(default_factory=EventLog)
@@ -1128,6 +1138,7 @@ class Colocation:
         m, P, cfg = self.m, self.pool, self.cfg
         self.res = RunResult(self.policy, {}, {})
         m.gpu_events = []
+        m.clock_n = 0
         log = self.res.log
         self.horizon_us = int(horizon_s * 1e6)
         P.reset()
@@ -1382,6 +1393,7 @@ class Colocation:
         self.online.synchronize()
         self.res.wall_s = time.perf_counter() - t0
         self.res.decode_gpu_us = [a.elapsed_time(b) * 1e3 for a, b in m.gpu_events]
+        self.res.decode_sm_mhz = m.clock_mhz[: m.clock_n].tolist()
         m.gpu_events = None
         end = now_us()
         if gc_was:
@@ -1608,6 +1620,7 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
                 r.log.write_jsonl(os.path.join(log_dir, f"{name}{i}.jsonl"))
                 with open(os.path.join(log_dir, f"{name}{i}_steps.json"), "w") as f:  # per-step device times
                     json.dump({"decode_gpu_us": [round(x, 1) for x in r.decode_gpu_us],
+                               "decode_sm_mhz": [round(x) for x in r.decode_sm_mhz],
                                "decode_iter_us": r.decode_iter_us, "prefill_us": r.prefill_us}, f)
 
     base_ttft, base_tpot = _med_runs([s.ttft_us for s in solos]), _med_runs([s.tpot_us for s in solos])
@@ -1642,6 +1655,7 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
             "decode_iter_ms_mean": sum(d for x in rs for d in x.decode_iter_us) / max(1, sum(len(x.decode_iter_us) for x in rs)) / 1e3,
             "step_gap_us_mean": sum(d for x in rs for d in x.step_gap_us) / max(1, sum(len(x.step_gap_us) for x in rs)),
             "decode_gpu_ms_mean": sum(d for x in rs for d in x.decode_gpu_us) / max(1, sum(len(x.decode_gpu_us) for x in rs)) / 1e3,
+            "decode_sm_mhz_mean": sum(d for x in rs for d in x.decode_sm_mhz) / max(1, sum(len(x.decode_sm_mhz) for x in rs)),
             "step_gap_us_p99": _pct([d for x in rs for d in x.step_gap_us], 99),
             "op_host_us_mean": {k: v / max(1, r.reclaims) for k, v in r.op_phase_us.items()},
             "quiesce_wait_us": {"p50": _pct(q, 50), "p99": _pct(q, 99), "max": max(q) if q else None, "n": len(q)},
@@ -1670,6 +1684,7 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
                        "decode_iter_ms_mean": sum(d for x in solos for d in x.decode_iter_us) / max(1, sum(len(x.decode_iter_us) for x in solos)) / 1e3,
                        "step_gap_us_mean": sum(d for x in solos for d in x.step_gap_us) / max(1, sum(len(x.step_gap_us) for x in solos)),
                        "decode_gpu_ms_mean": sum(d for x in solos for d in x.decode_gpu_us) / max(1, sum(len(x.decode_gpu_us) for x in solos)) / 1e3,
+                       "decode_sm_mhz_mean": sum(d for x in solos for d in x.decode_sm_mhz) / max(1, sum(len(x.decode_sm_mhz) for x in solos)),
                        "step_gap_us_p99": _pct([d for x in solos for d in x.step_gap_us], 99),
                        "plan_deviations": [_deviations(plan, x.plan) for x in solos],
                        "slow_iterations": {"n": sum(len(x.slow_iterations) for x in solos),

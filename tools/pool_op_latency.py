@@ -31,13 +31,15 @@ def main():
     arena = A.HostBuffer(12 << 30)
     gi = [0]
 
-    def tenant():
-        gate.reset_work()
-        gate.launch_offline(pool, None, None, 0, 0, None, ctas=16, stream=off.cuda_stream)
-        a, b, c, m, n, k, tiles = chain[gi[0] % len(chain)]
-        gi[0] += 1
-        ggate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, ctas=64, stream=gst.cuda_stream,
-                          fresh=True)
+    def tenant(decode=True, gemm=True):
+        if decode:
+            gate.reset_work()
+            gate.launch_offline(pool, None, None, 0, 0, None, ctas=16, stream=off.cuda_stream)
+        if gemm:
+            a, b, c, m, n, k, tiles = chain[gi[0] % len(chain)]
+            gi[0] += 1
+            ggate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, ctas=64,
+                              stream=gst.cuda_stream, fresh=True)
 
     def copies(n_ops):
         offs = 0
@@ -50,11 +52,11 @@ def main():
             pool.online_release(2)
 
     gen = [0]
-    for name, with_tenant, n_copy in (("idle", False, 0), ("tenant", True, 0), ("copies", False, 6),
-                                      ("tenant+copies", True, 6)):
+    for name, with_tenant, n_copy in (("idle", False, 0), ("decode_pass", "d", 0), ("gemm", "g", 0),
+                                      ("tenant", True, 0), ("copies", False, 6), ("tenant+copies", True, 6)):
         walls = []
         if with_tenant:
-            tenant()
+            tenant(decode=with_tenant in (True, "d"), gemm=with_tenant in (True, "g"))
         if n_copy:
             copies(n_copy)
         time.sleep(0.002)
@@ -66,7 +68,7 @@ def main():
             pool.offline_reserve(r, 200, 20_000 + i)
             w2 = time.perf_counter()
             walls += [(w1 - w0) * 1e6, (w2 - w1) * 1e6]
-            if with_tenant and ggate.read().live_ctas == 0:  # keep the GEMM chain busy
+            if with_tenant in (True, "g") and ggate.read().live_ctas == 0:  # keep the GEMM chain busy
                 a, b, c, m, n, k, tiles = chain[gi[0] % len(chain)]
                 gi[0] += 1
                 ggate.launch_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, ctas=64,
@@ -85,7 +87,8 @@ def main():
                 break
         torch.cuda.synchronize()
         print(json.dumps({"condition": name, "median_us": round(statistics.median(walls), 1),
-                          "p90_us": round(sorted(walls)[int(0.9 * len(walls))], 1), "max_us": round(max(walls), 1)}),
+                          "p90_us": round(sorted(walls)[int(0.9 * len(walls))], 1), "max_us": round(max(walls), 1),
+                          "argmax": walls.index(max(walls))}),
               flush=True)
 
 

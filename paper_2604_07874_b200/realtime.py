@@ -1493,7 +1493,7 @@ class _Clocks:
 
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,power.draw,temperature.gpu,temperature.memory",
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,power.draw,temperature.gpu,temperature.memory,clocks.mem",
                  "--format=csv,noheader,nounits", "-lms", "500"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
@@ -1527,7 +1527,7 @@ class _Clocks:
         pw = sorted(r[1] for r in self.rows)
         out = {"sm_mhz_median": sm[len(sm) // 2], "sm_mhz_min": sm[0], "power_w_median": pw[len(pw) // 2],
                "power_w_max": pw[-1], "samples": len(sm)}
-        for i, key in ((2, "gpu_temp_c"), (3, "mem_temp_c")):
+        for i, key in ((2, "gpu_temp_c"), (3, "mem_temp_c"), (4, "mem_mhz")):
             v = sorted(r[i] for r in self.rows if len(r) > i and r[i] == r[i])
             if v:
                 out[key + "_median"], out[key + "_max"] = v[len(v) // 2], v[-1]

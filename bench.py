@@ -391,14 +391,21 @@ def tp_fanout_across_ranks(torch, A, pool, dist, rank, world, gpu, groups=(2, 4,
             continue
         gate = A.Gate(gpu)
         grp = TP.TPGate(gate, rank, world, tp, dist, opener=TP.open_member(gpu))
-        lat = TP.measure_group_fanout(torch, gate, grp, pool, dist, gpu, iters=iters, seed=seed + rank)
+        lat, errs, viol = TP.measure_group_fanout(torch, gate, grp, pool, dist, gpu, iters=iters, seed=seed + rank)
+        if grp.error:
+            errs = [grp.error] + errs
         lat.sort()
-        mine = [lat[len(lat) // 2], lat[int(0.99 * (len(lat) - 1))], lat[-1]] if lat else [0.0, 0.0, 0.0]
-        t = torch.tensor(mine, device=torch.device("cuda", gpu), dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        out[str(tp)] = {"p50_us": round(t[0].item(), 2), "p99_us": round(t[1].item(), 2),
-                        "max_us": round(t[2].item(), 2), "preemptions_per_group": len(lat) if lat else iters,
-                        "groups": world // tp}
+        mine = {"lat": [lat[len(lat) // 2], lat[int(0.99 * (len(lat) - 1))], lat[-1]] if lat else None,
+                "errors": errs[:2], "not_quiesced": viol}
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+        lats = [x["lat"] for x in allr if x["lat"]]
+        out[str(tp)] = {"p50_us": round(max(x[0] for x in lats), 2) if lats else None,
+                        "p99_us": round(max(x[1] for x in lats), 2) if lats else None,
+                        "max_us": round(max(x[2] for x in lats), 2) if lats else None,
+                        "preemptions_per_group": iters, "groups": world // tp,
+                        "members_not_quiesced": sum(x["not_quiesced"] for x in allr),
+                        "errors": [e for x in allr for e in x["errors"]][:4]}
         del grp, gate
         dist.barrier()
     return {"note": "one process per GPU; leader raise -> every member's CTAs retired, over NVLink peer "
@@ -412,37 +419,53 @@ def c5_instances(torch, dist, gpu, rank, world, args):
     from paper_2604_07874_b200 import realtime as RT
 
     rcfg = RT.RtConfig(decode_ctas=args.rt_decode_ctas, gemm_ctas=args.rt_gemm_ctas)
-    r = RT.measure(horizon=args.rt_horizon_multi, tail_s=10.0, device=gpu, seed=args.seed + 101 * rank,
-                   repeats=1, cfg=rcfg, policies=())
-    v = r["valve"]
-    mine = {"rank": rank, "gpu": gpu, "online_requests": r["trace"]["online_requests"],
-            "ttft_delta_pct": v["ttft_delta_pct"], "tpot_delta_pct": v["tpot_delta_pct"],
-            "aa_noise_ttft_pct": r["aa_noise_ttft_pct"], "reclaims": v["reclaims"],
-            "offline_tokens_per_s": v["offline_tokens_per_s"], "quiesce_wait_us": v["quiesce_wait_us"]}
+    try:
+        r = RT.measure(horizon=args.rt_horizon_multi, tail_s=10.0, device=gpu, seed=args.seed + 101 * rank,
+                       repeats=1, cfg=rcfg, policies=(), handles=args.handles or 0)
+        v = r["valve"]
+        mine = {"rank": rank, "gpu": gpu, "online_requests": r["trace"]["online_requests"],
+                "ttft_delta_pct": v["ttft_delta_pct"], "tpot_delta_pct": v["tpot_delta_pct"],
+                "aa_noise_ttft_pct": r["aa_noise_ttft_pct"], "reclaims": v["reclaims"],
+                "offline_tokens_per_s": v["offline_tokens_per_s"], "quiesce_wait_us": v["quiesce_wait_us"]}
+    except Exception as e:  # noqa: BLE001 -- every rank must still reach the gather
+        mine = {"rank": rank, "gpu": gpu, "error": repr(e)[:300], "ttft_delta_pct": None, "tpot_delta_pct": None,
+                "offline_tokens_per_s": 0.0}
     allr = [None] * world
     dist.all_gather_object(allr, mine)
     return {"config": "C5: %d independent colocation instances (one per GPU), C2 spike trace per instance "
                       "(seed per rank), %.0f s horizon" % (world, args.rt_horizon_multi),
             "ranks": allr,
-            "ttft_delta_pct_max": max(x["ttft_delta_pct"] for x in allr if x["ttft_delta_pct"] is not None),
-            "tpot_delta_pct_max": max(x["tpot_delta_pct"] for x in allr if x["tpot_delta_pct"] is not None),
+            "ttft_delta_pct_max": max((x["ttft_delta_pct"] for x in allr if x["ttft_delta_pct"] is not None), default=None),
+            "tpot_delta_pct_max": max((x["tpot_delta_pct"] for x in allr if x["tpot_delta_pct"] is not None), default=None),
             "offline_tokens_per_s_total": sum(x["offline_tokens_per_s"] for x in allr)}
 
 
-def c4_tp(torch, dist, gpu, rank, world, args):
-    """C4 (configs[3]): Llama-3-70B TP = min(4, N) online groups over per-rank offline pools,
-    one group gate per TP group broadcast over NVLink peer memory (paper_2604_07874_b200.tp_colo)."""
-    from paper_2604_07874_b200 import tp as TP
-    from paper_2604_07874_b200 import tp_colo as C4
+def c4_job(world, args):
+    """C4 (configs[3]): Llama-3-70B TP = 4 (2 for N = 2, 6) online groups over per-rank offline
+    pools, one group gate per TP group broadcast over NVLink peer memory
+    (paper_2604_07874_b200.tp_colo via tools/c4_tp.py).  Launched by rank 0 as its own torchrun
+    job on the same GPUs once the bench's ranks have released their memory, under a timeout, so a
+    stuck collective there cannot take the bench's JSON line with it."""
+    import glob
+    import socket
+    import subprocess
 
     tp = 4 if world % 4 == 0 else 2
-    _, shared = TP.rank_device(int(os.environ.get("LOCAL_RANK", "0")),
-                               int(os.environ.get("LOCAL_WORLD_SIZE", str(world))), torch.cuda.device_count())
-    c = C4.C4Config(tp=tp, layers=args.c4_layers, horizon_s=args.c4_horizon)
-    r = C4.measure(dist, rank, world, gpu, shared, c, repeats=1)
-    allr = [None] * world
-    dist.all_gather_object(allr, r)
-    return {"groups": [x for x in allr if x is not None]}
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    out = os.path.join(ROOT, "gpurun_out", "c4", "c4.json")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    for f in glob.glob(os.path.join(os.path.dirname(out), "c4_g*.json")):
+        os.remove(f)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tools", "c4_tp.py"),
+           "--tp", str(tp), "--layers", str(args.c4_layers), "--horizon", str(args.c4_horizon), "--out", out]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    groups = [json.load(open(f)) for f in sorted(glob.glob(os.path.join(os.path.dirname(out), "c4_g*.json")))]
+    if r.returncode != 0 and not groups:
+        raise RuntimeError(f"c4 job rc={r.returncode}: {r.stderr[-300:]}")
+    return {"tp": tp, "groups": groups}
 
 
 VALVE_OPS = os.path.join(ROOT, "tools", "_bin", "valve_ops")
@@ -458,15 +481,25 @@ def e2e_cpp(torch, dist, gpu, H, args, world):
     import subprocess
 
     env = dict(os.environ, VALVE_DEVICE=str(gpu))
-    r = subprocess.run([VALVE_OPS, "e2e", str(H), str(args.k), str(max(1, args.steps)), str(max(1, args.warmup))],
-                       capture_output=True, text=True, timeout=600, env=env)
-    if r.returncode != 0:
-        raise RuntimeError(f"valve_ops e2e rc={r.returncode}: {r.stderr[-300:]}")
-    d = json.loads(r.stdout.strip().splitlines()[-1])
-    secs, nbytes = d["seconds"], d["bytes"]
-    if world > 1:
-        secs, nbytes = aggregate_ranks(dist, secs * 1e3, nbytes, torch.device("cuda", gpu))
-        secs *= 1e-3
+    d, err = None, None
+    try:
+        r = subprocess.run([VALVE_OPS, "e2e", str(H), str(args.k), str(max(1, args.steps)), str(max(1, args.warmup)),
+                            "0" if args.profile_mode else "1"], capture_output=True, text=True, timeout=600, env=env)
+        if r.returncode != 0:
+            raise RuntimeError(f"valve_ops e2e rc={r.returncode}: {r.stderr[-300:]}")
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 -- every rank must still reach the gather below
+        err = repr(e)[:300]
+    if world > 1:  # always gathered, so a failing rank cannot leave the others in a collective
+        allr = [None] * world
+        dist.all_gather_object(allr, (d["seconds"], d["bytes"]) if d else None)
+        if any(x is None for x in allr):
+            raise RuntimeError(err or "valve_ops e2e failed on another rank")
+        secs, nbytes = max(x[0] for x in allr), sum(x[1] for x in allr)
+    else:
+        if d is None:
+            raise RuntimeError(err)
+        secs, nbytes = d["seconds"], d["bytes"]
     return {"value": round(nbytes / secs / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": d["h2d_bytes_per_step"], "d2h_bytes_per_step": d["d2h_bytes_per_step"],
             "path": "C++: colosim::MemoryPool::snapshot() -> colosim::selective_reclaim() -> "
@@ -475,6 +508,11 @@ def e2e_cpp(torch, dist, gpu, H, args, world):
             "breakdown_ms_per_step": d["breakdown_ms_per_step"],
             "pipelining": "one reclaim copy queued behind the running one (op i+1 decides while op i copies); "
                           "the burst's first op preempts the offline tenant, which stays gated for the burst"}
+
+
+def _progress(rank, what):
+    """Phase marks on stderr (multi-rank runs: where a rank is when something stalls)."""
+    print(f"bench[{rank}] {time.strftime('%H:%M:%S')} {what}", file=sys.stderr, flush=True)
 
 
 def _guarded(name, fn):
@@ -494,6 +532,7 @@ def run_valve(args, rank, world, dist):
 
     dev = torch.device("cuda", torch.cuda.current_device())
     gpu = dev.index
+    _progress(rank, f"start on cuda:{gpu}")
     free, _ = torch.cuda.mem_get_info(dev)
     H = args.handles or min(1024, int((free - WEIGHTS - 6e9) // (SLOT * HSZ)))
     pool = A.DevicePool(H, HSZ, 16, device=gpu, slot_bytes=SLOT, page_bytes=PAGE,
@@ -626,6 +665,7 @@ def run_valve(args, rank, world, dist):
     if dist:
         elapsed_ms, total_bytes = aggregate_ranks(dist, elapsed_ms, total_bytes, dev)
 
+    _progress(rank, "timed burst done; preemption latency")
     # ------------------------------------------------ p50/p99 preempt-to-quiesce
     q = []
     gate.reset_work()
@@ -650,6 +690,7 @@ def run_valve(args, rank, world, dist):
     q = q or [float("nan")]
     pct = lambda p: q[min(len(q) - 1, int(round(p / 100 * (len(q) - 1))))]
 
+    _progress(rank, "polling overhead")
     # ------------------------------------------------ polling overhead (offline throughput)
     def offline_rate(poll):
         gate.reset_work()
@@ -668,6 +709,7 @@ def run_valve(args, rank, world, dist):
         polled = max(rates[True])
         unpolled = max(rates[False])
 
+    _progress(rank, "TP fan-out")
     # ------------------------------------------------ TP-group gate fan-out, one device
     fanout = None
     if not args.profile_mode and not args.skip_fanout and world == 1:
@@ -678,6 +720,7 @@ def run_valve(args, rank, world, dist):
         fanout = _guarded("tp_fanout", lambda: tp_fanout_across_ranks(torch, A, pool, dist, rank, world, gpu,
                                                                       seed=args.seed))
 
+    _progress(rank, "GEMM tenant")
     # ------------------------------------------------ GEMM tenant (tcgen05)
     def next_gen():
         gen[0] += 1
@@ -717,6 +760,7 @@ def run_valve(args, rank, world, dist):
         contrast[f"k{kk}"] = {"selective_tokens": sel_c, "fifo_tokens": fifo_c,
                               "reduction_pct": round((1 - sel_c / fifo_c) * 100, 2) if fifo_c else None}
 
+    _progress(rank, "e2e")
     # ------------------------------------------------ e2e through the reference-facing API
     # one copy stays in flight behind the running one (as in step()): op i+1's quiesce, snapshot,
     # selection and apply run on the host/pool stream while op i's bytes cross the link
@@ -773,6 +817,7 @@ def run_valve(args, rank, world, dist):
 
     copy_gbs = statistics.mean(b / (ms * 1e-3) / 1e9 for b, ms in zip(stats["bytes"], stats["copy_ms"]))
 
+    _progress(rank, "C3 + C++ e2e")
     # ------------------------------------------------ C3: weight pages (configs[2] mechanism)
     import gc
 
@@ -783,11 +828,12 @@ def run_valve(args, rank, world, dist):
     c3 = _guarded("c3_weight_pages", lambda: c3_weights(torch, A, gpu, cp, args.seed + rank, peak))
     cpp_e2e = _guarded("e2e_cpp", lambda: e2e_cpp(torch, dist, gpu, H, args, world))
 
+    _progress(rank, "real-time / C5 / C4")
     # ------------------------------------------------ measured online TTFT/TPOT deltas
     # (real-time loop: random-init Llama-3-8B online in PyTorch + the gated offline tenant on a
     # 32 GiB pool; the 128 GiB reclaim pool is released first)
     rt = {"note": "skipped (--skip-realtime)"}
-    c4 = None
+
     if world > 1 and not args.skip_realtime and not args.profile_mode:
         del gate
         gc.collect()
@@ -797,7 +843,7 @@ def run_valve(args, rank, world, dist):
         gc.collect()
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
-        c4 = _guarded("c4_tp_group", lambda: c4_tp(torch, dist, gpu, rank, world, args))
+        # C4 runs after this function, as its own torchrun job (main(): a hang there is contained)
     elif not args.skip_realtime and not args.profile_mode:
         del gate
         gc.collect()
@@ -862,7 +908,7 @@ def run_valve(args, rank, world, dist):
         "aa_noise_tpot_pct": rt.get("aa_noise_tpot_pct"),
         "shortfall_to_first_online_write_us": (rt.get("valve") or {}).get("shortfall_to_first_write_us"),
         "online_realtime": rt,
-        "c4_tp_group": c4 if c4 is not None else {"note": "runs at N >= 2 (one process per GPU)"},
+        "c4_tp_group": {"note": "runs at N >= 2 (one process per GPU)"},
         "roofline": {
             "bound": "pcie_d2h",
             "achieved": round(copy_gbs, 2),
@@ -1068,14 +1114,28 @@ def main():
         # NCCL with two ranks on one device, so it falls back to gloo for the plumbing
         import datetime
 
-        # a hung collective aborts the job after 10 minutes instead of holding the box
-        dist.init_process_group("gloo" if shared else "nccl", timeout=datetime.timedelta(seconds=600))
-        if shared and rank == 0:
-            print("bench: fewer GPUs than ranks -- ranks share devices; no number here is a multi-GPU number",
-                  file=sys.stderr, flush=True)
+        # a hung collective aborts the job after 30 minutes instead of holding the box (the C4
+        # job of up to 20 minutes runs while the other ranks wait in a barrier)
+        dist.init_process_group("gloo" if shared else "nccl", timeout=datetime.timedelta(seconds=1800))
+        if shared:
+            # two contexts time-slicing one GPU with persistent gated kernels make no meaningful
+            # (and a very slow) run: keep the replica burst + aggregation only, like --profile-mode
+            args.profile_mode = True
+            args.skip_realtime = args.skip_fanout = True
+            if rank == 0:
+                print("bench: fewer GPUs than ranks -- ranks share devices (functional run: no offline tenant, "
+                      "no TP / C4 / C5 legs); no number here is a multi-GPU number", file=sys.stderr, flush=True)
     else:
         torch.cuda.set_device(0)
     out = run_valve(args, rank, world, dist)
+    if dist is not None and not args.skip_realtime and not args.profile_mode:
+        # C4 as its own job on the same GPUs: every rank frees its memory and waits at a barrier
+        torch.cuda.empty_cache()
+        dist.barrier()
+        if rank == 0:
+            _progress(rank, "C4 job")
+            out["c4_tp_group"] = _guarded("c4_tp_group", lambda: c4_job(world, args))
+        dist.barrier()
     if rank == 0:
         try:
             out["cpu_baseline"] = cpu_baseline_block(args)

@@ -283,8 +283,40 @@ struct valve_pool {
 // instance and slot-collection passes' global reads use (200 KiB measured 3x slower collection)
 constexpr size_t kReclaimSmemBytes = 160 * 1024;
 
+// With CUDA's lazy module loading, a kernel's code is loaded at its first launch -- and that load
+// waits for the kernels already running on the device.  Under colocation the first
+// offline_release of a run can then sit behind a ~100 ms gated decode pass (measured: one 90 ms
+// pool op per process, gone under CUDA_MODULE_LOADING=EAGER).  Load every kernel of this library
+// up front instead (querying its attributes loads it), once per device, when the first pool /
+// gate / selection is created -- nothing is running yet at that point.
+static void preload_kernels(int device) {
+  static std::mutex mu;
+  static uint64_t done = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64 || (done >> device) & 1ull) return;
+  const void* ks[] = {
+      (const void*)k_online_grow, (const void*)k_online_release, (const void*)k_offline_reserve,
+      (const void*)k_offline_release, (const void*)k_ht_rehash, (const void*)k_requests_on_handle,
+      (const void*)k_handles_of_request, (const void*)k_offline_pages_of, (const void*)k_block_table,
+      (const void*)k_snapshot_handles, (const void*)k_snapshot, (const void*)k_apply, (const void*)k_reclaim_rows,
+      (const void*)k_reclaim, (const void*)k_reclaim_fused, (const void*)k_check_invariants,
+      (const void*)k_fill_pages, (const void*)k_set_costs, (const void*)k_select_instance, (const void*)k_map_refs,
+      (const void*)k_tile_prefix, (const void*)k_evicted_cost, (const void*)k_reclaim_copy,
+      (const void*)k_copy_plan, (const void*)k_reclaim_copy_tma, (const void*)k_restore_scatter,
+      (const void*)k_gate_raise_stamp, (const void*)k_offline_decode, (const void*)k_offline_gemm,
+      (const void*)k_offline_gemm_pair};
+  for (const void* k : ks) {
+    cudaFuncAttributes a{};
+    ck(cudaFuncGetAttributes(&a, k), "load kernel");
+  }
+  done |= 1ull << device;
+}
+
 static void set_reclaim_smem_attrs() {
   // per device, per process (cheap to repeat)
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  preload_kernels(dev);
   ck(cudaFuncSetAttribute(k_reclaim_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 32768),
      "cudaFuncSetAttribute");
   ck(cudaFuncSetAttribute(k_reclaim_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kReclaimSmemBytes),
@@ -412,6 +444,9 @@ static void pool_init(valve_pool* p, const valve_pool_config& c) {
     d.pages = static_cast<uint8_t*>(pg);
   }
   ck(cudaHostAlloc((void**)&p->mirror, sizeof(Mirror), cudaHostAllocMapped), "cudaHostAlloc");
+  // result staging sized for a whole-pool snapshot / report now: a first-use cudaHostAlloc inside
+  // a reclaim on the online critical path took milliseconds
+  p->stage((size_t)H * 16 + (size_t)H * S * 16 + (size_t)R * 16 + 64);
   ck(cudaHostGetDevicePointer((void**)&d.mirror, p->mirror, 0), "cudaHostGetDevicePointer");
   pool_reset_state(p);
   // dynamic shared memory: greedy marginals (2048 handles) aliased with the apply sort
@@ -1784,6 +1819,7 @@ int valve_gate_create(int device, valve_gate** out) {
     g->device = device;
     try {
       ck(cudaSetDevice(device), "cudaSetDevice");
+      preload_kernels(device);
       int lo = 0, hi = 0;
       ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
       ck(cudaStreamCreateWithPriority(&g->stream, cudaStreamNonBlocking, hi), "stream");

@@ -59,10 +59,15 @@ class TPGate:
         handles = [None] * world
         dist.all_gather_object(handles, gate.export())
         self.members = []
+        self.error = None
         if self.is_leader:
-            self.members = [opener(handles[r]) for r in self.group if r != rank]
-            if self.members:
-                gate.attach_peers(self.members)
+            try:
+                self.members = [opener(handles[r]) for r in self.group if r != rank]
+                if self.members:
+                    gate.attach_peers(self.members)
+            except Exception as e:  # noqa: BLE001 -- recorded; every rank still reaches the barrier
+                self.error = repr(e)[:200]
+                self.members = []
         dist.barrier()
 
     # leader-side controls (members never drive the group gate)
@@ -99,39 +104,60 @@ def measure_group_fanout(torch, gate, group: "TPGate", pool, dist, device: int, 
     memory operations on every member's words over peer memory) and its stream waits until every
     member's CTAs retired.  Latency = CUDA events around raise + wait on the leader's gate
     stream.  Iterations are host-synchronised with dist.barrier() so every member is running
-    when the leader raises.  Returns the leader's samples (members: []).  The reference's
-    unpatched toggle is linear in the GPUs (scenario.hpp:56-58)."""
+    when the leader raises.  The reference's unpatched toggle is linear in the GPUs
+    (scenario.hpp:56-58, PAPER.md:366-373).
+
+    Every rank runs the same barrier schedule whatever happens on its device (a failing call is
+    recorded, not raised), so one rank's error cannot leave the others inside a collective.
+    Returns (leader's samples in us, errors, members seen not quiesced after the wait)."""
     import random
 
     rng = random.Random(seed)
     off = torch.cuda.Stream(device=device)
     gs = torch.cuda.ExternalStream(gate.stream, device=device)
-    lat = []
+    lat, errors, violations = [], [], 0
+
+    def attempt(fn):
+        if len(errors) > 3:  # a broken path: stop touching the device, keep the schedule
+            return False
+        try:
+            fn()
+            return True
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e)[:200])
+            return False
+
     for it in range(iters + 10):
-        gate.reset_work()
-        gate.launch_offline(pool, None, None, 0, 0, None, ctas=ctas, stream=off.cuda_stream)
-        torch.cuda.synchronize(device)  # the launch is queued and its CTAs start
+        def start():
+            gate.reset_work()
+            gate.launch_offline(pool, None, None, 0, 0, None, ctas=ctas, stream=off.cuda_stream)
+        attempt(start)
+        time.sleep(0.001)  # the pass is running (it lasts far longer than a sample)
         dist.barrier()
         if group.is_leader:
-            deadline = time.perf_counter() + rng.uniform(100e-6, 400e-6)
-            while time.perf_counter() < deadline:
-                pass
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(gs)
-            group.raise_(it + 1)
-            group.wait_quiesced(it + 1)
-            e1.record(gs)
-            e1.synchronize()
-            if it >= 10:
-                lat.append(e0.elapsed_time(e1) * 1e3)
+            def sample():
+                deadline = time.perf_counter() + rng.uniform(100e-6, 400e-6)
+                while time.perf_counter() < deadline:
+                    pass
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(gs)
+                group.raise_(it + 1)
+                group.wait_quiesced(it + 1)
+                e1.record(gs)
+                e1.synchronize()
+                if it >= 10:
+                    lat.append(e0.elapsed_time(e1) * 1e3)
+            attempt(sample)
         dist.barrier()
-        st = gate.read()
-        assert st.closed == 1 and st.live_ctas == 0, (group.rank, st.closed, st.live_ctas)
+
+        def check():
+            nonlocal violations
+            st = gate.read()
+            violations += int(not (st.closed == 1 and st.live_ctas == 0))
+        attempt(check)
         dist.barrier()
         if group.is_leader:
-            group.release(it + 1)
-            gs.synchronize()
+            attempt(lambda: (group.release(it + 1), gs.synchronize()))
         dist.barrier()
-        gate.cancel_work()  # drop the rest of the pass: the next sample starts a fresh one
-        off.synchronize()
-    return lat
+        attempt(lambda: (gate.cancel_work(), off.synchronize()))  # next sample: a fresh pass
+    return lat, errors, violations

@@ -12,7 +12,7 @@
 //   ops table H k1,k2,..           per-op latency (median us): offline_reserve, offline_release,
 //                                  and snapshot -> selective_reclaim -> apply_reclaim for each k;
 //                                  valve_ops adds the fused device op (valve_pool_reclaim)
-//   ops e2e H k steps warmup       (valve_ops) bench.py's e2e leg in C++: per op raise the gate and
+//   ops e2e H k steps warmup [tenant] (valve_ops) bench.py's e2e leg in C++: per op raise the gate and
 //                                  wait for the offline decode pass to quiesce, snapshot, select,
 //                                  apply, start the gather copy of the invalidated pages into
 //                                  pinned host memory, re-admit; one copy queued behind the
@@ -205,7 +205,7 @@ void table(int H, const std::vector<int>& ks) {
 }
 
 #ifdef VALVE_DROPIN
-void e2e(int H, int k, int steps, int warmup) {
+void e2e(int H, int k, int steps, int warmup, bool tenant) {
   MemoryPool pool = make_pool(H, true);
   Population pop;
   pool.online_grow((H + 9) / 10, 0);
@@ -250,7 +250,7 @@ void e2e(int H, int k, int steps, int warmup) {
     }
     ++gen;
     auto p0 = clk::now();
-    if (it == 0 || it == warmup) {  // a burst's first op preempts the running offline tenant
+    if (tenant && (it == 0 || it == warmup)) {  // a burst's first op preempts the running offline tenant
       valve_detail::check(valve_offline_reset(gate));
       valve_detail::check(valve_offline_launch(gate, pool.native(), &w, off_stream));
     }
@@ -338,7 +338,7 @@ int main(int argc, char** argv) {
 #ifdef VALVE_DROPIN
     if (mode == "e2e") {
       e2e(argc > 2 ? std::atoi(argv[2]) : 1024, argc > 3 ? std::atoi(argv[3]) : 36, argc > 4 ? std::atoi(argv[4]) : 20,
-          argc > 5 ? std::atoi(argv[5]) : 3);
+          argc > 5 ? std::atoi(argv[5]) : 3, argc > 6 ? std::atoi(argv[6]) != 0 : true);
       return 0;
     }
 #endif

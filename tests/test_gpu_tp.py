@@ -1,5 +1,6 @@
-"""TP-group gate fan-out across processes, on one GPU: two processes (a TP group
-of 2) share cuda:0; the member's gate words are opened by the leader through CUDA IPC and
+"""TP-group gate fan-out across processes: two processes (a TP group of 2), rank r on
+cuda:r (sharing cuda:0 on a 1-GPU box); the member's gate words are opened by the leader through
+CUDA IPC (peer memory across GPUs) and
 driven with stream memory operations.  The member's gated offline kernel must quiesce on the
 leader's raise (leader waits on the member's live_ctas), keep its context (cursor), and resume
 to completion after the leader's release -- every tile exactly once."""
@@ -30,12 +31,13 @@ def _worker(rank, port, q):
     from paper_2604_07874_b200 import tp as TP
 
     dist.init_process_group("gloo", rank=rank, world_size=2)
-    torch.cuda.set_device(0)
-    gate = A.Gate(0)
-    group = TP.TPGate(gate, rank, 2, 2, dist, opener=lambda h: A.Gate.open_remote(h, 0))
+    gpu, _ = TP.rank_device(rank, 2, torch.cuda.device_count())  # cuda:rank on a multi-GPU box
+    torch.cuda.set_device(gpu)
+    gate = A.Gate(gpu)
+    group = TP.TPGate(gate, rank, 2, 2, dist, opener=TP.open_member(gpu))
     out = {"rank": rank}
     if rank == 1:  # member: a long offline pass over its own pool
-        pool = A.DevicePool(64, 16, 16, slot_bytes=1 << 20, page_bytes=917504)
+        pool = A.DevicePool(64, 16, 16, device=gpu, slot_bytes=1 << 20, page_bytes=917504)
         for r in range(64):
             pool.offline_reserve(r, 16, 0)
         pool.fill_pages()

@@ -1,12 +1,14 @@
-"""TP-group gate fan-out latency vs group size, one process per member, all on one GPU (the only
-multi-process topology this run has).  Every member runs its gated offline kernel; the leader
-raises the group gate (stream memops on every member's words through CUDA IPC) and waits for
-every member's CTAs to retire.  Prints one JSON line per group size."""
+"""TP-group gate fan-out latency vs group size, one process per member (rank r on cuda:r when the
+box has a GPU per rank; on a 1-GPU box the members share the device -- functional only).  Every
+member runs its gated offline kernel; the leader raises the group gate (stream memops on every
+member's words through CUDA IPC / NVLink peer memory) and waits for every member's CTAs to retire
+(paper_2604_07874_b200.tp.measure_group_fanout).  Prints one JSON line per group size."""
 import json
 import os
 import socket
 import sys
-import time
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # before any CUDA context
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch.multiprocessing as mp  # noqa: E402
@@ -28,40 +30,22 @@ def worker(rank, world, port, iters, q):
     from paper_2604_07874_b200 import api as A
     from paper_2604_07874_b200 import tp as TP
 
+    gpu, shared = TP.rank_device(rank, world, torch.cuda.device_count())
+    torch.cuda.set_device(gpu)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    torch.cuda.set_device(0)
-    gate = A.Gate(0)
-    grp = TP.TPGate(gate, rank, world, world, dist, opener=lambda h: A.Gate.open_remote(h, 0))
-    pool = A.DevicePool(32, 16, 16, slot_bytes=1 << 20, page_bytes=917504)
-    for r in range(32):
+    gate = A.Gate(gpu)
+    grp = TP.TPGate(gate, rank, world, world, dist, opener=TP.open_member(gpu))
+    pool = A.DevicePool(512, 16, 16, device=gpu, slot_bytes=1 << 20, page_bytes=917504)  # a pass of ~7 GB
+    for r in range(512):
         pool.offline_reserve(r, 16, 0)
     pool.fill_pages()
-    s = torch.cuda.Stream()
-    lat = []
-    for it in range(iters):
-        gate.reset_work()
-        gate.launch_offline(pool, None, None, 0, 0, None, ctas=max(1, 64 // world), stream=s.cuda_stream)
-        dist.barrier()
-        if grp.is_leader:
-            time.sleep(0.0003)
-            gs = torch.cuda.ExternalStream(gate.stream)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(gs)
-            grp.raise_(it + 1)
-            grp.wait_quiesced(it + 1)
-            e1.record(gs)
-            e1.synchronize()
-            lat.append(e0.elapsed_time(e1) * 1e3)
-        dist.barrier()
-        if grp.is_leader:
-            grp.release(it + 1)
-            torch.cuda.synchronize()
-        dist.barrier()
-        s.synchronize()
+    lat, errs, viol = TP.measure_group_fanout(torch, gate, grp, pool, dist, gpu, iters=iters,
+                                              ctas=max(1, 64 // world), seed=rank)
     if grp.is_leader:
         lat.sort()
-        q.put({"group": world, "p50_us": lat[len(lat) // 2], "p99_us": lat[int(0.99 * (len(lat) - 1))],
-               "max_us": lat[-1], "iters": iters})
+        q.put({"group": world, "shared_device": shared, "p50_us": lat[len(lat) // 2] if lat else None,
+               "p99_us": lat[int(0.99 * (len(lat) - 1))] if lat else None, "max_us": lat[-1] if lat else None,
+               "iters": iters, "errors": errs[:2], "not_quiesced": viol})
     dist.barrier()
     dist.destroy_process_group()
 
@@ -71,10 +55,10 @@ def main():
     for world in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,2,4,8").split(",")]:
         q = ctx.Queue()
         port = _port()
-        ps = [ctx.Process(target=worker, args=(r, world, port, 200, q)) for r in range(world)]
+        ps = [ctx.Process(target=worker, args=(r, world, port, 100, q)) for r in range(world)]
         for p in ps:
             p.start()
-        print(json.dumps(q.get(timeout=600)), flush=True)
+        print(json.dumps(q.get(timeout=900)), flush=True)
         for p in ps:
             p.join(120)
 

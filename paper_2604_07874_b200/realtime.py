@@ -1022,7 +1022,8 @@ class Colocation:
                 return 0
             head_off = self._copies[0][1]
             tail_end = self._copies[-1][1] + self._copies[-1][2]
-            if tail_end >= head_off:  # in-flight bytes [head_off, tail_end): free tail, then wrap to 0
+            # (a non-wrapped ring has tail_end > head_off; tail_end == head_off is a wrapped, full ring)
+            if tail_end > head_off:  # in-flight bytes [head_off, tail_end): free tail, then wrap to 0
                 if tail_end + nbytes <= size:
                     return tail_end
                 if nbytes <= head_off:

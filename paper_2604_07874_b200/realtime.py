@@ -683,6 +683,8 @@ class RunResult:
     step_gap_us: List[float] = field(default_factory=list)  # host time between back-to-back busy steps
     decode_gpu_us: List[float] = field(default_factory=list)  # device time of each decode graph replay
     decode_sm_mhz: List[float] = field(default_factory=list)  # SM clock at the start of each replay
+    decode_t_us: List[int] = field(default_factory=list)  # loop time at the start of each decode step
+    busy_starts: List[int] = field(default_factory=list)  # loop time of every busy edge
     slow_iterations: List[dict] = field(default_factory=list)  # loop iterations with > 3 ms host time
     deferred_releases: int = 0  # MIAD releases postponed: no copied-out slots to move the KV into
     log: EventLog = field(default_factory=EventLog)
@@ -1306,6 +1308,7 @@ class Colocation:
             if not busy:  # busy edge: raise + wait for the offline CTAs to retire (sim.cpp:362-369)
                 busy = self._busy = True
                 busy_since = now
+                self.res.busy_starts.append(now)
                 if self.colocated:
                     self._harvest(now, force=True)
                     self.channel.note_busy(now)
@@ -1363,6 +1366,7 @@ class Colocation:
             marks.append(("alloc", pc()))
             slow_check("decode")
             t_it = now_us()
+            self.res.decode_t_us.append(t_it)
             if gap_from is not None:
                 self.res.step_gap_us.append(t_it - gap_from)
             with torch.cuda.stream(self.online):
@@ -1622,6 +1626,7 @@ def measure(horizon=60.0, base=2.0, spike=20.0, period=6.0, width=1.0, prompt=(2
                 with open(os.path.join(log_dir, f"{name}{i}_steps.json"), "w") as f:  # per-step device times
                     json.dump({"decode_gpu_us": [round(x, 1) for x in r.decode_gpu_us],
                                "decode_sm_mhz": [round(x) for x in r.decode_sm_mhz],
+                               "decode_t_us": r.decode_t_us, "busy_starts": r.busy_starts,
                                "decode_iter_us": r.decode_iter_us, "prefill_us": r.prefill_us}, f)
 
     base_ttft, base_tpot = _med_runs([s.ttft_us for s in solos]), _med_runs([s.tpot_us for s in solos])

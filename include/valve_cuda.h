@@ -140,8 +140,9 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
  * build (snapshot), out[1] selection, out[2] apply; out[3..4] SM cycles of the greedy rounds
  * (argmin, incremental update); out[5..8] apply sub-phases (evicted rows + ranks, report order,
  * residual release, request-table erase), out[9..11] (validation, slot collection, per-handle
- * ranks) of the last apply in this process.  Diagnostics. */
-int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[12]);
+ * ranks) of the last apply, out[12..15] selection sub-phases (dense request ids, CSR + reverse
+ * index, packed-key checks, rounds) of the last selection in this process.  Diagnostics. */
+int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[16]);
 int valve_pool_last_reclaim(const valve_pool* p, int* handles, int64_t* evicted, int* inv_off,
                             int64_t* inv_pages, int* inv_phys, int* inv_blk, int cap_h, int cap_ev,
                             int cap_pages);

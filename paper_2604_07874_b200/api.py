@@ -883,7 +883,7 @@ class DevicePool(MemoryPool):
 
     def reclaim_phases_us(self):
         """(instance, select, apply) device microseconds of the last reclaim()."""
-        out = _arr(i64, 12)
+        out = _arr(i64, 16)
         self._b.check(self._b.lib.valve_pool_reclaim_phases(self._h, _ptr(out, i64)))
         return out[0] / 1e3, out[1] / 1e3, out[2] / 1e3
 

@@ -26,6 +26,7 @@ static_assert(kSmemTuples * 20 <= 160 * 1024, "sort smem");
 static_assert((1024 + 3 * 8192 + 6 * 2048) * 4 <= 160 * 1024, "apply fast-path smem");  // key 8 + pay 4 + cursors 4 + segment 4
 
 __device__ long long g_greedy_cycles[2];  // diagnostics: argmin / update cycles of the last run
+__device__ long long g_select_ns[5];      // diagnostics: selection phase stamps of the last run
 __device__ long long g_apply_ns[10];       // diagnostics: apply_core phase stamps of the last run
 
 // Ref lists of instance handle i: CSR (off) or fixed stride with counts (cnt), the stride slot
@@ -355,6 +356,7 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
                               const int64_t* cost, int k, int64_t* marg_g, int* taken_g, int* ev,
                               int* qoff, int* qcnt, int* qh, int* out, unsigned char* smem,
                               int* dense = nullptr) {
+  if (threadIdx.x == 0) g_select_ns[0] = (long long)globaltimer_ns();
   int nnz_local = 0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) nnz_local += R.end(i) - R.begin(i);
   const int nnz = block_sum(nnz_local);
@@ -378,6 +380,7 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
       __syncthreads();
       m2 = s_m2;
       qcnt = dense;
+      if (threadIdx.x == 0) g_select_ns[1] = (long long)globaltimer_ns();
     } else {
       // dense request index over the referenced requests (qcnt: flag -> dense id)
       for (int r = threadIdx.x; r < m; r += blockDim.x) qcnt[r] = 0;
@@ -457,6 +460,7 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
       marg[i] = s;
     }
     __syncthreads();
+    if (threadIdx.x == 0) g_select_ns[2] = (long long)globaltimer_ns();
     // packed-key rounds when ids ascend, costs are >= 0 and the marginals fit the key
     int idbits = 1;
     while ((1 << idbits) < n) ++idbits;
@@ -481,6 +485,7 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
     const int qmax = has_dup ? 0 : s_qmax;
     const Refs Rs{roff, nullptr, 0};
     unsigned* skey = reinterpret_cast<unsigned*>(taken + kSmemHandles);
+    if (threadIdx.x == 0) g_select_ns[3] = (long long)globaltimer_ns();
     if (packed && n <= 1024) {
       if (threadIdx.x < 32) greedy_warp_packed(n, hid, Rs, rr, cost2, k, marg, skey, ev2, qoff2, qh2, out, idbits, qmax);
     } else if (threadIdx.x < kGreedyThreads) {
@@ -490,6 +495,7 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
     if (dense)
       for (int d = threadIdx.x; d < m2; d += blockDim.x) dense[qoff[d]] = -1;  // back to all -1
     __syncthreads();
+    if (threadIdx.x == 0) g_select_ns[4] = (long long)globaltimer_ns();
   } else {
     build_instance_index(n, R, rref, m, cost, marg_g, qoff, qcnt, qh, ev);
     greedy_cta(n, hid_g, R, rref, cost, k, marg_g, taken_g, ev, qoff, qh, out);

@@ -1072,7 +1072,7 @@ int valve_pool_reclaim(valve_pool* p, int k, int mode, int64_t t, int* n_handles
   });
 }
 
-int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[12]) {
+int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[16]) {
   const int64_t* r = p->mirror->r;
   out[0] = r[4] - r[3];
   out[1] = r[5] - r[4];
@@ -1090,6 +1090,12 @@ int valve_pool_reclaim_phases(const valve_pool* p, int64_t out[12]) {
   out[9] = an[6] - an[5];  // validation of the pick
   out[10] = an[7] > an[6] ? an[7] - an[6] : 0;  // slot collection + clear (fast path)
   out[11] = an[8] > an[7] ? an[8] - an[7] : 0;  // per-handle ranks + pairs (fast path)
+  long long sn[5] = {0, 0, 0, 0, 0};
+  cudaMemcpyFromSymbol(sn, valve::g_select_ns, sizeof sn);
+  out[12] = sn[1] > sn[0] ? sn[1] - sn[0] : 0;  // selection: dense request ids
+  out[13] = sn[2] > sn[1] ? sn[2] - sn[1] : 0;  //   CSR listings + reverse index + marginals
+  out[14] = sn[3] > sn[2] ? sn[3] - sn[2] : 0;  //   packed-key / duplicate checks
+  out[15] = sn[4] > sn[3] ? sn[4] - sn[3] : 0;  //   the k rounds
   return VALVE_OK;
 }
 

@@ -49,6 +49,7 @@ __global__ void k_tile_prefix(const int* npages, int n, int cpp, int64_t* prefix
                               unsigned long long* total_out, unsigned* frozen);
 __global__ void k_evicted_cost(SelectArgs A, const int* pick, int n_pick);
 extern __device__ long long g_greedy_cycles[2];
+extern __device__ long long g_select_ns[5];
 extern __device__ long long g_apply_ns[10];
 
 // reclaim copy (copy_kernels.cu)

@@ -14,7 +14,8 @@ from paper_2604_07874_b200 import api as A  # noqa: E402
 
 NAMES = ["instance_us", "select_us", "apply_us", "argmin_cycles", "update_cycles",
          "apply_evrows_us", "apply_sort_us", "apply_release_us", "apply_erase_us",
-         "apply_validate_us", "apply_collect_us", "apply_rank_us"]
+         "apply_validate_us", "apply_collect_us", "apply_rank_us",
+         "select_dense_us", "select_csr_us", "select_checks_us", "select_rounds_us"]
 
 
 def main(k=36, H=1024, reps=20):
@@ -29,9 +30,9 @@ def main(k=36, H=1024, reps=20):
         w0 = time.perf_counter()
         pool.reclaim(k, t + 10 * i, 0)
         wall.append((time.perf_counter() - w0) * 1e6)
-        out = (C.c_int64 * 12)()
+        out = (C.c_int64 * 16)()
         f(pool.handle, out)
-        rows.append([out[j] / 1e3 if j not in (3, 4) else out[j] for j in range(12)])
+        rows.append([out[j] / 1e3 if j not in (3, 4) else out[j] for j in range(16)])
         res = pool.last_reclaim()
         pool.online_release(k)
         for r in res.evicted_requests:

@@ -473,9 +473,10 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
     // flat update rounds need distinct requests within every handle's listings (the fused
     // path's rows are deduplicated; host instances may repeat a request on a handle)
     int dup = 0, qm = 0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x)
-      for (int o = roff[i]; o < roff[i + 1]; ++o)
-        for (int o2 = roff[i]; o2 < o; ++o2) dup |= rr[o2] == rr[o];
+    if (!dense)  // the fused path's rows come from warp_distinct_rows: no quadratic check
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        for (int o = roff[i]; o < roff[i + 1]; ++o)
+          for (int o2 = roff[i]; o2 < o; ++o2) dup |= rr[o2] == rr[o];
     for (int d = threadIdx.x; d < m2; d += blockDim.x) qm = max(qm, qoff2[d + 1] - qoff2[d]);
     __shared__ int s_qmax;
     if (threadIdx.x == 0) s_qmax = 0;

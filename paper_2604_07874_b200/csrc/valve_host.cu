@@ -500,14 +500,16 @@ namespace {
 // filled with `fill` bytes (or left uninitialised for scratch when fill < 0).
 template <class T>
 void regrow(valve_pool* p, T*& ptr, int64_t keep, int64_t n, int fill) {
+  // stream-ordered allocation: cudaMalloc / cudaFree may synchronize the whole device, which
+  // would wait for (and deadlock on) a gated tenant's stream parked behind a closed gate
   void* np = nullptr;
-  ck(cudaMalloc(&np, std::max<int64_t>(n, 1) * sizeof(T)), "cudaMalloc(table growth)");
+  ck(cudaMallocAsync(&np, std::max<int64_t>(n, 1) * sizeof(T), p->stream), "cudaMallocAsync(table growth)");
   if (fill >= 0) ck(cudaMemsetAsync(np, fill, n * sizeof(T), p->stream), "memset");
   if (keep > 0) ck(cudaMemcpyAsync(np, ptr, keep * sizeof(T), cudaMemcpyDeviceToDevice, p->stream), "copy");
-  ck(cudaStreamSynchronize(p->stream), "table growth");
   auto it = std::find(p->dev_allocs.begin(), p->dev_allocs.end(), static_cast<void*>(ptr));
   if (it != p->dev_allocs.end()) *it = np;
-  cudaFree(ptr);
+  if (ptr) ck(cudaFreeAsync(ptr, p->stream), "cudaFreeAsync(table growth)");
+  ck(cudaStreamSynchronize(p->stream), "table growth");
   ptr = static_cast<T*>(np);
 }
 
@@ -529,14 +531,14 @@ void grow_tables(valve_pool* p, int R2, int P2) {
   const int64_t HS = (int64_t)p->H * p->S;
   if (P2 != P || R2 != R) {  // block tables: new pitch and/or more rows
     int* nbt = nullptr;
-    ck(cudaMalloc((void**)&nbt, (size_t)R2 * P2 * 4), "cudaMalloc(block tables)");
+    ck(cudaMallocAsync((void**)&nbt, (size_t)R2 * P2 * 4, p->stream), "cudaMallocAsync(block tables)");
     ck(cudaMemsetAsync(nbt, 0xff, (size_t)R2 * P2 * 4, p->stream), "memset");
     ck(cudaMemcpy2DAsync(nbt, (size_t)P2 * 4, d.bt, (size_t)P * 4, (size_t)P * 4, R, cudaMemcpyDeviceToDevice,
                          p->stream), "copy");
-    ck(cudaStreamSynchronize(p->stream), "table growth");
     auto it = std::find(p->dev_allocs.begin(), p->dev_allocs.end(), static_cast<void*>(d.bt));
     if (it != p->dev_allocs.end()) *it = nbt;
-    cudaFree(d.bt);
+    ck(cudaFreeAsync(d.bt, p->stream), "cudaFreeAsync(block tables)");
+    ck(cudaStreamSynchronize(p->stream), "table growth");
     d.bt = nbt;
   }
   if (P2 != P) regrow(p, p->d_ids, 0, std::max<int64_t>(std::max(p->H, 1) * 2, P2), -1);
@@ -585,8 +587,8 @@ void grow_tables(valve_pool* p, int R2, int P2) {
     const int HC = d.HC;
     int* nrow = nullptr;
     int64_t* nkey = nullptr;
-    ck(cudaMalloc((void**)&nrow, (size_t)HC2 * 4), "cudaMalloc(request hash)");
-    ck(cudaMalloc((void**)&nkey, (size_t)HC2 * 8), "cudaMalloc(request hash)");
+    ck(cudaMallocAsync((void**)&nrow, (size_t)HC2 * 4, p->stream), "cudaMallocAsync(request hash)");
+    ck(cudaMallocAsync((void**)&nkey, (size_t)HC2 * 8, p->stream), "cudaMallocAsync(request hash)");
     ck(cudaMemsetAsync(nrow, 0xff, (size_t)HC2 * 4, p->stream), "memset");
     d.ht_row = nrow;
     d.ht_key = nkey;
@@ -602,8 +604,9 @@ void grow_tables(valve_pool* p, int R2, int P2) {
       if (a == old_row) a = nrow;
       else if (a == old_key) a = nkey;
     }
-    cudaFree(old_row);
-    cudaFree(old_key);
+    ck(cudaFreeAsync(old_row, p->stream), "cudaFreeAsync(request hash)");
+    ck(cudaFreeAsync(old_key, p->stream), "cudaFreeAsync(request hash)");
+    ck(cudaStreamSynchronize(p->stream), "rehash");
   }
   d.P = P2;
   p->Pblk = P2;
@@ -1507,10 +1510,12 @@ struct SelectCtx {
   int64_t* result = nullptr;
   std::mutex mu;
 
+  // stream-ordered (see regrow): a device-synchronizing cudaFree here would wait for a gated
+  // tenant's stream parked behind a closed gate -- the host that would reopen it is in here
   template <class T>
   void grow(T*& ptr, int64_t n) {
-    if (ptr) cudaFree(ptr);
-    ck(cudaMalloc((void**)&ptr, std::max<int64_t>(n, 1) * sizeof(T)), "cudaMalloc");
+    if (ptr) ck(cudaFreeAsync(ptr, stream), "cudaFreeAsync");
+    ck(cudaMallocAsync((void**)&ptr, std::max<int64_t>(n, 1) * sizeof(T), stream), "cudaMallocAsync");
   }
   void reserve(int64_t n, int64_t nnz, int64_t m) {
     if (!stream) ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");

@@ -14,8 +14,12 @@ REF_OPS = os.path.join(ROOT, "oracle", "_ref", "ref_ops")
 VALVE_OPS = os.path.join(ROOT, "tools", "_bin", "valve_ops")
 
 
-def _run(exe, *args, env=None):
-    r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=600, env=env)
+def _run(exe, *args, env=None, timeout=600):
+    try:
+        r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=timeout, env=env)
+    except subprocess.TimeoutExpired as e:  # show how far the driver got (VALVE_OPS_TRACE)
+        err = e.stderr.decode() if isinstance(e.stderr, bytes) else (e.stderr or "")
+        raise AssertionError(f"{exe} {' '.join(args)} timed out after {timeout} s; stderr tail:\n{err[-3000:]}")
     assert r.returncode == 0, r.stderr[-2000:]
     return json.loads(r.stdout.strip().splitlines()[-1])
 
@@ -47,6 +51,6 @@ def test_table_same_reclaims_as_reference():
 
 @pytest.mark.gpu
 def test_e2e_leg_moves_the_reported_bytes():
-    d = _run(VALVE_OPS, "e2e", "128", "8", "3", "1")
+    d = _run(VALVE_OPS, "e2e", "128", "8", "3", "1", env=dict(os.environ, VALVE_OPS_TRACE="1"), timeout=180)
     assert d["steps"] == 3 and d["bytes"] > 0 and d["gbs"] > 1.0
     assert d["d2h_bytes_per_step"] >= d["bytes"] // 3

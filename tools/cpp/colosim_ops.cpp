@@ -238,6 +238,10 @@ void e2e(int H, int k, int steps, int warmup, bool tenant) {
     return got;
   };
   std::uint32_t gen = 0;
+  const bool trace = std::getenv("VALVE_OPS_TRACE") != nullptr;
+  auto mark = [&](int it, const char* what) {
+    if (trace) std::fprintf(stderr, "e2e it %d: %s\n", it, what), std::fflush(stderr);
+  };
   auto t_start = clk::now();
   for (int it = 0; it < warmup + steps; ++it) {
     if (it == warmup) {  // timed burst starts: drain the warm-up, reopen, preempt again
@@ -254,9 +258,11 @@ void e2e(int H, int k, int steps, int warmup, bool tenant) {
       valve_detail::check(valve_offline_reset(gate));
       valve_detail::check(valve_offline_launch(gate, pool.native(), &w, off_stream));
     }
+    mark(it, "raise");
     valve_detail::check(valve_gate_raise(gate, gen, nullptr));
     valve_detail::check(valve_gate_wait_quiesced(gate, gen, nullptr));
     valve_detail::check(valve_stream_synchronize(valve_gate_stream(gate)));
+    mark(it, "quiesced");
     auto p1 = clk::now();
     ReclaimInstance inst = pop.instance(pool);
     auto p2 = clk::now();
@@ -264,6 +270,7 @@ void e2e(int H, int k, int steps, int warmup, bool tenant) {
     auto p3 = clk::now();
     MemoryPool::ReclaimResult rr = pool.apply_reclaim(pick, ++pop.t);
     auto p4 = clk::now();
+    mark(it, "applied");
     std::int64_t npg = 0;
     for (const auto& kv : rr.invalidated_pages) npg += static_cast<std::int64_t>(kv.second.size());
     valve_detail::check(valve_pool_reclaim_copy_start(pool.native(), host[it % 2], cap, &cp));
@@ -271,7 +278,9 @@ void e2e(int H, int k, int steps, int warmup, bool tenant) {
     auto p5 = clk::now();
     pop.restore(pool, static_cast<int>(rr.handles.size()), rr.evicted_requests);
     auto p6 = clk::now();
+    mark(it, "restored");
     bytes += drain(1);
+    mark(it, "drained");
     auto p7 = clk::now();
     std::int64_t nnz = 0;
     for (const ReclaimHandle& h : inst.handles) nnz += static_cast<std::int64_t>(h.requests.size());

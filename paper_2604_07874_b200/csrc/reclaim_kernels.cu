@@ -368,15 +368,25 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
       __shared__ int s_m2;
       if (threadIdx.x == 0) s_m2 = 0;
       __syncthreads();
-      for (int i = threadIdx.x; i < n; i += blockDim.x)
-        for (int e = R.begin(i); e < R.end(i); ++e) {
-          const int r = rref[e];
-          if (atomicCAS(&dense[r], -1, -2) == -1) {
-            const int d = atomicAdd(&s_m2, 1);
-            dense[r] = d;
-            qoff[d] = r;  // dense id -> row, for the reset
-          }
+      // 8 listings per batch: the row loads, then the claims, are issued back to back (one
+      // L2 round trip each per batch instead of per listing)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int b = R.begin(i), c = R.end(i) - b;
+        for (int e0 = 0; e0 < c; e0 += 8) {
+          int r[8], old[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) r[u] = e0 + u < c ? rref[b + e0 + u] : -1;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) old[u] = r[u] >= 0 ? atomicCAS(&dense[r[u]], -1, -2) : 0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (old[u] == -1) {
+              const int d = atomicAdd(&s_m2, 1);
+              dense[r[u]] = d;
+              qoff[d] = r[u];  // dense id -> row, for the reset
+            }
         }
+      }
       __syncthreads();
       m2 = s_m2;
       qcnt = dense;
@@ -427,14 +437,25 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
       qcnt2[d] = 0;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      int o = roff[i];
-      for (int e = R.begin(i); e < R.end(i); ++e, ++o) {
-        const int r = rref[e];
-        const int d = qcnt[r];
-        rr[o] = d;
-        cost2[d] = cost[r];
-        atomicAdd(&qcnt2[d], 1);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {  // batches of 8 listings (as above)
+      const int b = R.begin(i), c = R.end(i) - b, o = roff[i];
+      for (int e0 = 0; e0 < c; e0 += 8) {
+        int r[8], d[8];
+        int64_t cr[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = e0 + u < c ? rref[b + e0 + u] : -1;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          d[u] = r[u] >= 0 ? qcnt[r[u]] : -1;
+          cr[u] = r[u] >= 0 ? cost[r[u]] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (d[u] >= 0) {
+            rr[o + e0 + u] = d[u];
+            cost2[d[u]] = cr[u];
+            atomicAdd(&qcnt2[d[u]], 1);
+          }
       }
     }
     __syncthreads();
@@ -608,7 +629,10 @@ __device__ __forceinline__ void warp_sort_asc(uint64_t* key, int* pay, int n, in
 // reference mutates handle by handle and throws at the first bad one), reports the
 // invalidated pages sorted per request, and -- if the whole list was valid -- releases the
 // residual pages of every evicted request.  Writes res_* and the mirror counts.
-__device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, unsigned char* smem) {
+// `trusted`: ids are distinct offline handles by construction (the fused path's own picks), so
+// the reference's per-handle validation (memory.cpp:158-161) cannot fail and is skipped.
+__device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, unsigned char* smem,
+                           bool trusted = false) {
   __shared__ int s_bad, s_nt, s_freed;
   if (threadIdx.x == 0) {
     g_apply_ns[5] = (long long)globaltimer_ns();
@@ -617,7 +641,7 @@ __device__ void apply_core(const PoolDev& P, const int* ids, int k, int64_t t, u
     s_freed = 0;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+  for (int i = threadIdx.x; i < k && !trusted; i += blockDim.x) {
     const int h = ids[i];
     bool bad = h < 0 || h >= P.H || P.hstate[h] != kOffline;
     for (int j = 0; j < i && !bad; ++j) bad = ids[j] == h;
@@ -1151,7 +1175,7 @@ __device__ void reclaim_body(const PoolDev& P, int k, int mode, int64_t t, unsig
   }
   __syncthreads();
   if (threadIdx.x == 0) P.mirror->r[5] = (int64_t)globaltimer_ns();
-  apply_core(P, P.s_pick, k, t, smem);
+  apply_core(P, P.s_pick, k, t, smem, /*trusted=*/true);
   __syncthreads();
   if (threadIdx.x == 0) P.mirror->r[6] = (int64_t)globaltimer_ns();
   publish(P);

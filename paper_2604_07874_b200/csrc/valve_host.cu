@@ -131,6 +131,9 @@ struct valve_pool {
   int64_t* d_in64b = nullptr;
   size_t smem_snapshot = 0, smem_reclaim = 0;
   std::vector<void*> dev_allocs;
+  // block tables replaced by growth: a gated offline launch already enqueued (possibly parked
+  // behind a closed gate) holds the old pointer, so the old table lives until the pool does
+  std::vector<void*> retired_bt;
   int last_n_handles = 0, last_n_evicted = 0, last_n_pages = 0;
   int64_t last_copy_bytes = 0;  // destination bytes of the last report (per-request page sizes)
   int last_custom = 0;          // some evicted request has its own page size
@@ -264,6 +267,7 @@ struct valve_pool {
     for (cudaStream_t s : {plan_stream, copy_stream, stream})
       if (s) cudaStreamSynchronize(s);
     for (void* p : dev_allocs) cudaFree(p);
+    for (void* p : retired_bt) cudaFree(p);
     if (d.pages) cudaFree(d.pages);
     if (mirror) cudaFreeHost(mirror);
     if (hst) cudaFreeHost(hst);
@@ -537,8 +541,8 @@ void grow_tables(valve_pool* p, int R2, int P2) {
                          p->stream), "copy");
     auto it = std::find(p->dev_allocs.begin(), p->dev_allocs.end(), static_cast<void*>(d.bt));
     if (it != p->dev_allocs.end()) *it = nbt;
-    ck(cudaFreeAsync(d.bt, p->stream), "cudaFreeAsync(block tables)");
     ck(cudaStreamSynchronize(p->stream), "table growth");
+    p->retired_bt.push_back(d.bt);  // not freed: see retired_bt
     d.bt = nbt;
   }
   if (P2 != P) regrow(p, p->d_ids, 0, std::max<int64_t>(std::max(p->H, 1) * 2, P2), -1);
@@ -564,7 +568,7 @@ void grow_tables(valve_pool* p, int R2, int P2) {
     regrow(p, d.s_ev, 0, R2, 0);
     regrow(p, d.s_qoff, 0, R2 + 1, -1);
     regrow(p, d.s_qcnt, 0, std::max<int64_t>(HS, R2), -1);
-    regrow(p, d.s_dense, 0, R2, -1);
+    regrow(p, d.s_dense, 0, R2, 0xff);  // -1 everywhere between selections (greedy_select)
     regrow(p, d.s_evrows, 0, R2, -1);
     regrow(p, d.s_rank, 0, R2, -1);
     regrow(p, d.res_evicted, R, R2, 0);

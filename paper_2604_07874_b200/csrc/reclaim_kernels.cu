@@ -368,25 +368,15 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
       __shared__ int s_m2;
       if (threadIdx.x == 0) s_m2 = 0;
       __syncthreads();
-      // 8 listings per batch: the row loads, then the claims, are issued back to back (one
-      // L2 round trip each per batch instead of per listing)
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int b = R.begin(i), c = R.end(i) - b;
-        for (int e0 = 0; e0 < c; e0 += 8) {
-          int r[8], old[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) r[u] = e0 + u < c ? rref[b + e0 + u] : -1;
-#pragma unroll
-          for (int u = 0; u < 8; ++u) old[u] = r[u] >= 0 ? atomicCAS(&dense[r[u]], -1, -2) : 0;
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (old[u] == -1) {
-              const int d = atomicAdd(&s_m2, 1);
-              dense[r[u]] = d;
-              qoff[d] = r[u];  // dense id -> row, for the reset
-            }
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        for (int e = R.begin(i); e < R.end(i); ++e) {
+          const int r = rref[e];
+          if (atomicCAS(&dense[r], -1, -2) == -1) {
+            const int d = atomicAdd(&s_m2, 1);
+            dense[r] = d;
+            qoff[d] = r;  // dense id -> row, for the reset
+          }
         }
-      }
       __syncthreads();
       m2 = s_m2;
       qcnt = dense;
@@ -437,25 +427,14 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
       qcnt2[d] = 0;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {  // batches of 8 listings (as above)
-      const int b = R.begin(i), c = R.end(i) - b, o = roff[i];
-      for (int e0 = 0; e0 < c; e0 += 8) {
-        int r[8], d[8];
-        int64_t cr[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) r[u] = e0 + u < c ? rref[b + e0 + u] : -1;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          d[u] = r[u] >= 0 ? qcnt[r[u]] : -1;
-          cr[u] = r[u] >= 0 ? cost[r[u]] : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (d[u] >= 0) {
-            rr[o + e0 + u] = d[u];
-            cost2[d[u]] = cr[u];
-            atomicAdd(&qcnt2[d[u]], 1);
-          }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      int o = roff[i];
+      for (int e = R.begin(i); e < R.end(i); ++e, ++o) {
+        const int r = rref[e];
+        const int d = qcnt[r];
+        rr[o] = d;
+        cost2[d] = cost[r];
+        atomicAdd(&qcnt2[d], 1);
       }
     }
     __syncthreads();

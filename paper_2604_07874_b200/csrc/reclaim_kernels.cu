@@ -357,8 +357,14 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
                               int* qoff, int* qcnt, int* qh, int* out, unsigned char* smem,
                               int* dense = nullptr) {
   if (threadIdx.x == 0) g_select_ns[0] = (long long)globaltimer_ns();
+  // this thread's handle's listing range, read once: inside the loops below the compiler cannot
+  // hoist Refs' global words (map, counts) past the atomics, so it would re-read them per listing
+  const int tb = (int)threadIdx.x < n ? R.begin(threadIdx.x) : 0;
+  const int te = (int)threadIdx.x < n ? R.end(threadIdx.x) : 0;
+  auto rb = [&](int i) { return i == (int)threadIdx.x ? tb : R.begin(i); };
+  auto re = [&](int i) { return i == (int)threadIdx.x ? te : R.end(i); };
   int nnz_local = 0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) nnz_local += R.end(i) - R.begin(i);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) nnz_local += re(i) - rb(i);
   const int nnz = block_sum(nnz_local);
   if (n <= kSmemHandles && nnz <= kSmemListings) {
     int m2 = 0;
@@ -369,7 +375,7 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
       if (threadIdx.x == 0) s_m2 = 0;
       __syncthreads();
       for (int i = threadIdx.x; i < n; i += blockDim.x)
-        for (int e = R.begin(i); e < R.end(i); ++e) {
+        for (int e = rb(i), ee = re(i); e < ee; ++e) {
           const int r = rref[e];
           if (atomicCAS(&dense[r], -1, -2) == -1) {
             const int d = atomicAdd(&s_m2, 1);
@@ -386,7 +392,7 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
       for (int r = threadIdx.x; r < m; r += blockDim.x) qcnt[r] = 0;
       __syncthreads();
       for (int i = threadIdx.x; i < n; i += blockDim.x)
-        for (int e = R.begin(i); e < R.end(i); ++e) qcnt[rref[e]] = 1;
+        for (int e = rb(i), ee = re(i); e < ee; ++e) qcnt[rref[e]] = 1;
       __syncthreads();
       for (int base = 0; base < m; base += blockDim.x) {
         const int r = base + threadIdx.x;
@@ -411,7 +417,7 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
     int carry = 0;
     for (int base = 0; base < n; base += blockDim.x) {
       const int i = base + threadIdx.x;
-      const int c = i < n ? R.end(i) - R.begin(i) : 0;
+      const int c = i < n ? re(i) - rb(i) : 0;
       int tot;
       const int ex = block_excl_scan(c, tot);
       if (i < n) {
@@ -429,7 +435,7 @@ __device__ void greedy_select(int n, const int* hid_g, Refs R, const int* rref, 
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       int o = roff[i];
-      for (int e = R.begin(i); e < R.end(i); ++e, ++o) {
+      for (int e = rb(i), ee = re(i); e < ee; ++e, ++o) {
         const int r = rref[e];
         const int d = qcnt[r];
         rr[o] = d;

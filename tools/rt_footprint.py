@@ -46,11 +46,11 @@ def main(reps=8):
     def sweep(kind):
         if kind == "large":
             for c in big.view(torch.int64).split((1 << 30) // 8):  # 48 x 1 GB chunks, each once
-                torch.sum(c, dtype=torch.int64, out=sink)
+                torch.sum(c, dim=0, dtype=torch.int64, out=sink)
         elif kind == "small":
             v = small.view(torch.int64)
             for _ in range(48):
-                torch.sum(v, dtype=torch.int64, out=sink)
+                torch.sum(v, dim=0, dtype=torch.int64, out=sink)
 
     g = torch.cuda.CUDAGraph()
     step()

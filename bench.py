@@ -534,6 +534,7 @@ def run_valve(args, rank, world, dist):
     gpu = dev.index
     _progress(rank, f"start on cuda:{gpu}")
     free, _ = torch.cuda.mem_get_info(dev)
+    free = free / getattr(args, "ranks_per_device", 1)
     H = args.handles or min(1024, int((free - WEIGHTS - 6e9) // (SLOT * HSZ)))
     pool = A.DevicePool(H, HSZ, 16, device=gpu, slot_bytes=SLOT, page_bytes=PAGE,
                         max_requests=4096, max_pages_per_request=1024)
@@ -1122,6 +1123,9 @@ def main():
             # (and a very slow) run: keep the replica burst + aggregation only, like --profile-mode
             args.profile_mode = True
             args.skip_realtime = args.skip_fanout = True
+            # the ranks on one device split its memory (each would otherwise size a full pool)
+            args.ranks_per_device = -(-int(os.environ.get("LOCAL_WORLD_SIZE", str(world))) //
+                                      max(1, torch.cuda.device_count()))
             if rank == 0:
                 print("bench: fewer GPUs than ranks -- ranks share devices (functional run: no offline tenant, "
                       "no TP / C4 / C5 legs); no number here is a multi-GPU number", file=sys.stderr, flush=True)

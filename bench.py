@@ -33,6 +33,7 @@ the same pages, on this box's host cores.
 import argparse
 import ctypes as C
 import json
+import math
 import os
 import random
 import statistics
@@ -523,6 +524,17 @@ def _guarded(name, fn):
     except Exception as e:  # noqa: BLE001
         print(f"bench: {name} failed: {e!r}", file=sys.stderr, flush=True)
         return {"error": repr(e)[:300]}
+
+
+def _finite(o):
+    """NaN / inf (e.g. an empty sample's percentile) -> null: the line stays strict JSON."""
+    if isinstance(o, float):
+        return o if math.isfinite(o) else None
+    if isinstance(o, dict):
+        return {k: _finite(v) for k, v in o.items()}
+    if isinstance(o, (list, tuple)):
+        return [_finite(v) for v in o]
+    return o
 
 
 def run_valve(args, rank, world, dist):
@@ -1099,7 +1111,7 @@ def main():
     dist = None
     if args.impl == "reference":
         if rank == 0:
-            print(json.dumps(run_reference(args, rank, world)), flush=True)
+            print(json.dumps(_finite(run_reference(args, rank, world))), flush=True)
         return
     import torch
 
@@ -1145,7 +1157,7 @@ def main():
             out["cpu_baseline"] = cpu_baseline_block(args)
         except Exception as e:  # the checker must never block the device number
             out["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
-        print(json.dumps(out), flush=True)
+        print(json.dumps(_finite(out)), flush=True)
     if dist:
         dist.destroy_process_group()
 
